@@ -1,0 +1,181 @@
+/*
+ * bf.h -- C ABI of libbf200.so: bulk add / contains over blocked Bloom filters
+ * on NVIDIA B200 (sm_100a).  Implements the data-parallel hot path of
+ * arXiv 2512.15595 ("Optimizing Bloom Filters for Modern GPU Architectures").
+ *
+ * Citations: P:Lnnn = /root/reference/PAPER.md line nnn (the paper);
+ *            S:Lnnn = /root/reference/SPEC.md line nnn;
+ *            DESIGN.md section 2 = the hash and layout spec this library and the
+ *            independent CPU oracle (oracle/) both implement.
+ *
+ * Conventions for every entry point:
+ *   - Plain C types only.  "device pointer" = a CUDA global-memory pointer valid
+ *     on the filter's device (e.g. torch.Tensor.data_ptr() of a CUDA tensor);
+ *     "host pointer" = ordinary (ideally pinned) host memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     All device work is enqueued on `stream` and the call returns without
+ *     synchronizing, unless stated otherwise.
+ *   - Return value: BF_OK (0) or a negative BF_E* code.  Invalid arguments are
+ *     detected synchronously, before any work is enqueued, and return
+ *     BF_EINVAL.  A failed CUDA call returns BF_ECUDA.  bf_last_error() gives
+ *     the code and a message for the calling thread's most recent failure.
+ *   - Ownership: the library owns the filter's word array (allocated in
+ *     bf_create, freed in bf_destroy).  The caller owns every key / result
+ *     buffer and must keep it alive until `stream` has consumed it.
+ *   - n == 0 is a no-op returning BF_OK.
+ *   - Keys are uint64 ("unique, random uint64_t input keys"), 8-byte
+ *     aligned.  32-byte-aligned key arrays take the 256-bit-load fast path.
+ */
+#ifndef BF_H
+#define BF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Filter variants; numbering follows S:L272.
+ *   BF_CBF  classical Bloom filter -- oracle only: bf_create
+ *           returns NULL with BF_EUNSUPPORTED.
+ *   BF_BBF  blocked: all k bits inside one B-bit block.
+ *   BF_RBBF register-blocked: B == S, one word per key.
+ *   BF_SBF  sectorized: block = s = B/S words, k/s bits per word.
+ *   BF_CSBF cache-sectorized: s words in z groups, one word per
+ *           group selected, k/z bits in it.  z travels in bits 8..15 of
+ *           `variant`: BF_CSBF_Z(z). */
+enum { BF_CBF = 0, BF_BBF = 1, BF_RBBF = 2, BF_SBF = 3, BF_CSBF = 4 };
+#define BF_CSBF_Z(z) (BF_CSBF | ((uint32_t)(z) << 8))
+
+enum {
+    BF_OK = 0,
+    BF_EINVAL = -1,        /* invalid argument / configuration              */
+    BF_ENOMEM = -2,        /* device or host allocation failed              */
+    BF_ECUDA = -3,         /* a CUDA runtime call or kernel launch failed   */
+    BF_EUNSUPPORTED = -4   /* valid request this build does not implement   */
+};
+
+typedef struct bf_filter bf_filter; /* opaque */
+
+/* Create a zero-filled filter on the current CUDA device ("a bit array
+ * of size m"; blocks P:L117, words P:L127, groups P:L132).
+ *   m_bits     requested size in bits, >= 1; the filter holds b = ceil(m/B)
+ *              blocks (m_eff = b*B bits; b <= 2^32).
+ *   k          bits per key, 1..32.
+ *   block_bits B in {32, 64, 128, 256, 512, 1024}, >= word_bits.
+ *   word_bits  S in {32, 64}: the atomic / compare unit.
+ *   variant    BF_BBF | BF_RBBF (needs B == S) | BF_SBF (needs k % s == 0) |
+ *              BF_CSBF_Z(z) (needs z | s, k % z == 0, z <= 16).
+ * Allocation is cudaMalloc (>= 256-byte aligned) + synchronous cudaMemset.
+ * Returns NULL on error (bf_last_error: BF_EINVAL / BF_ENOMEM / BF_ECUDA /
+ * BF_EUNSUPPORTED). */
+bf_filter* bf_create(uint64_t m_bits, uint32_t k, uint32_t block_bits,
+                     uint32_t word_bits, uint32_t variant);
+
+/* Same, with an explicit XXH64 seed (default 0). */
+bf_filter* bf_create_seeded(uint64_t m_bits, uint32_t k, uint32_t block_bits,
+                            uint32_t word_bits, uint32_t variant, uint64_t seed);
+
+/* Bulk insert (P:L245 steps (1)-(2); "the corresponding bits are set to
+ * one").  keys: device pointer to n uint64.  Sets the k pattern bits of every
+ * key with red.global.or; concurrent bf_add calls on any streams are safe
+ * (OR commutes).  Idempotent. */
+int bf_add(bf_filter* f, const uint64_t* keys, uint64_t n, void* stream);
+
+/* Bulk lookup ("If any bit is zero, the element is certainly not in the
+ * set"; P:L245 step (3) "results are written back in a coalesced fashion").
+ * keys: device pointer to n uint64.  out_bits: device pointer to ceil(n/32)
+ * uint32; bit (i % 32) of word (i / 32) = contains(keys[i]) (LSB-first); bits
+ * past n in the last word are written 0.  A contains racing an add on the
+ * same filter has no guarantee for keys in flight. */
+int bf_contains(const bf_filter* f, const uint64_t* keys, uint64_t n,
+                uint32_t* out_bits, void* stream);
+
+/* Host-buffer variants (end-to-end path): keys / out_bits are HOST pointers.
+ * The library streams them through internal device staging buffers in
+ * chunks, overlapping the host->device copies with the kernels on `stream`.
+ * These calls synchronize `stream` before returning (the host result is
+ * ready on return). */
+int bf_add_host(bf_filter* f, const uint64_t* host_keys, uint64_t n, void* stream);
+int bf_contains_host(const bf_filter* f, const uint64_t* host_keys, uint64_t n,
+                     uint32_t* host_out_bits, void* stream);
+
+/* Zero the filter (cudaMemsetAsync on stream). */
+int bf_clear(bf_filter* f, void* stream);
+
+/* Free the filter.  NULL-safe.  The caller must have synchronized every
+ * stream that still uses it. */
+void bf_destroy(bf_filter* f);
+
+/* Raw word array (device pointer) and its size in bytes = b*B/8.  The memory
+ * layout is DESIGN.md section 2: bit p of block i is bit p%8 of byte
+ * i*B/8 + p/8.  Used by parity tests and the multi-GPU merge. */
+int bf_data(const bf_filter* f, void** dev_words, uint64_t* bytes);
+
+/* Geometry: b blocks, s words per block, m_eff = b*B bits.  Any out pointer
+ * may be NULL. */
+int bf_geometry(const bf_filter* f, uint64_t* b, uint32_t* s, uint64_t* m_eff_bits);
+
+/* Choose the kernel schedule (P:L159-219 vectorization layouts, P:L241-252
+ * cooperation; P:L228-237 hash variants).  Results never depend on it.
+ *   op            0 = add, 1 = contains
+ *   theta         Θ: lanes cooperating on one key (power of two)
+ *   phi           Φ: contiguous words per lane per step (power of two);
+ *                 1 <= Θ·Φ <= s
+ *   kpt           keys per thread: 1, 2 or 4
+ *   hash_variant  0 salts as immediates / per-thread registers,
+ *                 1 salts from a __constant__ table, 2 from a shared-memory
+ *                 table, 3 every lane re-hashes its group's key (no shuffle)
+ * theta = 0 restores the default schedule (contains Θ=1, Φ=s; add Θ=s, Φ=1).
+ * Returns BF_EINVAL for an invalid layout, BF_EUNSUPPORTED if that schedule
+ * is not compiled for this (variant, B, S, k, z). */
+int bf_set_layout(bf_filter* f, int op, int theta, int phi, int kpt, int hash_variant);
+
+/* Current schedule of `op` and whether it runs a specialized (compile-time
+ * k/B/S) kernel (1) or the generic runtime-parameter kernel (0). */
+int bf_get_layout(const bf_filter* f, int op, int* theta, int* phi, int* kpt,
+                  int* hash_variant, int* specialized);
+
+/* dst[i] = OR over r < nsrc of src_r[i], for `bytes` bytes (multiple of 8).
+ * srcs: device pointer to nsrc arrays laid out src_stride_bytes apart (the
+ * receive buffer of an all-gather); dst may alias src_0.  The merge step of a
+ * replicated multi-GPU build (NCCL has no bitwise-OR reduction).  HBM
+ * streaming: reads nsrc*bytes, writes bytes. */
+int bf_or_fold(void* dst, const void* srcs, uint32_t nsrc, uint64_t src_stride_bytes,
+               uint64_t bytes, void* stream);
+
+/* out[i] = mix64(base_index + i) (SplitMix64 output function), i < n: the
+ * synthetic key generator of DESIGN.md section 5 on the device.  out: device
+ * pointer, 8-byte aligned. */
+int bf_keygen(uint64_t* out, uint64_t n, uint64_t base_index, void* stream);
+
+/* Roofline probes: the filter's access pattern without hashing
+ * or pattern generation.  For each key, block = ((key >> 32) * b) >> 32 over
+ * a buffer of b blocks of block_bits bits.
+ *   probe_read: loads the whole block with the widest load, AND-reduces it and
+ *               writes one ballot-packed bit per key to out_bits (like
+ *               bf_contains).
+ *   probe_red:  `lanes` lanes (1 .. block_bits/64) each issue one 64-bit
+ *               red.global.or of a key-derived bit into their word of the
+ *               block (like bf_add with Θ = lanes).
+ * buf: device pointer to b*block_bits/8 bytes. */
+int bf_probe_read(const void* buf, uint64_t b, uint32_t block_bits, const uint64_t* keys,
+                  uint64_t n, uint32_t* out_bits, void* stream);
+int bf_probe_red(void* buf, uint64_t b, uint32_t block_bits, uint32_t lanes,
+                 const uint64_t* keys, uint64_t n, void* stream);
+
+/* Number of kernels this library has launched since load (all entry points).
+ * Lets callers prove the CUDA path ran. */
+uint64_t bf_launch_count(void);
+
+/* Code and message of the calling thread's most recent failure (code may be
+ * NULL).  Returns "" and BF_OK if none. */
+const char* bf_last_error(int* code);
+
+/* Library version string. */
+const char* bf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BF_H */

@@ -1,0 +1,259 @@
+"""Thin Python binding of libbf200.so (include/bf.h), same names as the C ABI.
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels behind the C ABI.  torch is used for device memory and streams
+(``tensor.data_ptr()``, ``torch.cuda.current_stream().cuda_stream``).
+
+There is no fallback: if the library is missing this module raises on import
+(build it with ``python -m paper_2512_15595_b200.build`` or
+``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbf200.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "bf.h")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: the CUDA library has not been built "
+                      "(run __graft_entry__.build()); there is no CPU fallback")
+
+_lib = C.CDLL(LIB_PATH)
+
+BF_CBF, BF_BBF, BF_RBBF, BF_SBF, BF_CSBF = 0, 1, 2, 3, 4
+BF_OK, BF_EINVAL, BF_ENOMEM, BF_ECUDA, BF_EUNSUPPORTED = 0, -1, -2, -3, -4
+VARIANTS = {"BBF": BF_BBF, "RBBF": BF_RBBF, "SBF": BF_SBF, "CSBF": BF_CSBF}
+OP_ADD, OP_CONTAINS = 0, 1
+
+
+def BF_CSBF_Z(z: int) -> int:
+    return BF_CSBF | (z << 8)
+
+
+_u64, _u32, _i32, _vp = C.c_uint64, C.c_uint32, C.c_int, C.c_void_p
+_SIGS = {
+    "bf_create": (_vp, [_u64, _u32, _u32, _u32, _u32]),
+    "bf_create_seeded": (_vp, [_u64, _u32, _u32, _u32, _u32, _u64]),
+    "bf_add": (_i32, [_vp, _vp, _u64, _vp]),
+    "bf_contains": (_i32, [_vp, _vp, _u64, _vp, _vp]),
+    "bf_add_host": (_i32, [_vp, _vp, _u64, _vp]),
+    "bf_contains_host": (_i32, [_vp, _vp, _u64, _vp, _vp]),
+    "bf_clear": (_i32, [_vp, _vp]),
+    "bf_destroy": (None, [_vp]),
+    "bf_data": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_u64)]),
+    "bf_geometry": (_i32, [_vp, C.POINTER(_u64), C.POINTER(_u32), C.POINTER(_u64)]),
+    "bf_set_layout": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32]),
+    "bf_get_layout": (_i32, [_vp, _i32] + [C.POINTER(_i32)] * 5),
+    "bf_or_fold": (_i32, [_vp, _vp, _u32, _u64, _u64, _vp]),
+    "bf_keygen": (_i32, [_vp, _u64, _u64, _vp]),
+    "bf_probe_read": (_i32, [_vp, _u64, _u32, _vp, _u64, _vp, _vp]),
+    "bf_probe_red": (_i32, [_vp, _u64, _u32, _u32, _vp, _u64, _vp]),
+    "bf_launch_count": (_u64, []),
+    "bf_last_error": (C.c_char_p, [C.POINTER(_i32)]),
+    "bf_version": (C.c_char_p, []),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+def declared_symbols() -> list[str]:
+    """Every function include/bf.h declares."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]*?\b(bf_\w+)\s*\(", txt, re.M)))
+
+
+class BFError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"bf error {code}: {msg}")
+        self.code = code
+
+
+def last_error() -> tuple[int, str]:
+    c = _i32()
+    msg = _lib.bf_last_error(C.byref(c))
+    return int(c.value), (msg or b"").decode()
+
+
+def _check(rc: int) -> int:
+    if rc != BF_OK:
+        code, msg = last_error()
+        raise BFError(rc, msg)
+    return rc
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return int(getattr(stream, "cuda_stream", stream))
+
+
+def _ptr(x) -> int:
+    return int(x.data_ptr()) if hasattr(x, "data_ptr") else int(x)
+
+
+# ---------------------------------------------------------------- C names
+def bf_create(m_bits: int, k: int, block_bits: int, word_bits: int, variant: int, seed: int = 0) -> int:
+    h = _lib.bf_create_seeded(m_bits, k, block_bits, word_bits, variant, seed)
+    if not h:
+        code, msg = last_error()
+        raise BFError(code, msg)
+    return h
+
+
+def bf_add(f: int, keys, n: int | None = None, stream=None) -> None:
+    n = keys.numel() if n is None else n
+    _check(_lib.bf_add(f, _ptr(keys), n, _stream(stream)))
+
+
+def bf_contains(f: int, keys, out_bits, n: int | None = None, stream=None) -> None:
+    n = keys.numel() if n is None else n
+    _check(_lib.bf_contains(f, _ptr(keys), n, _ptr(out_bits), _stream(stream)))
+
+
+def bf_add_host(f: int, host_keys, n: int | None = None, stream=None) -> None:
+    n = host_keys.numel() if n is None else n
+    _check(_lib.bf_add_host(f, _ptr(host_keys), n, _stream(stream)))
+
+
+def bf_contains_host(f: int, host_keys, host_out_bits, n: int | None = None, stream=None) -> None:
+    n = host_keys.numel() if n is None else n
+    _check(_lib.bf_contains_host(f, _ptr(host_keys), n, _ptr(host_out_bits), _stream(stream)))
+
+
+def bf_clear(f: int, stream=None) -> None:
+    _check(_lib.bf_clear(f, _stream(stream)))
+
+
+def bf_destroy(f: int) -> None:
+    _lib.bf_destroy(f)
+
+
+def bf_data(f: int) -> tuple[int, int]:
+    p, nb = _vp(), _u64()
+    _check(_lib.bf_data(f, C.byref(p), C.byref(nb)))
+    return int(p.value or 0), int(nb.value)
+
+
+def bf_geometry(f: int) -> tuple[int, int, int]:
+    b, s, m = _u64(), _u32(), _u64()
+    _check(_lib.bf_geometry(f, C.byref(b), C.byref(s), C.byref(m)))
+    return int(b.value), int(s.value), int(m.value)
+
+
+def bf_set_layout(f: int, op: int, theta: int, phi: int, kpt: int = 1, hash_variant: int = 0) -> None:
+    _check(_lib.bf_set_layout(f, op, theta, phi, kpt, hash_variant))
+
+
+def bf_get_layout(f: int, op: int) -> dict:
+    v = [_i32() for _ in range(5)]
+    _check(_lib.bf_get_layout(f, op, *[C.byref(x) for x in v]))
+    return dict(zip(("theta", "phi", "kpt", "hash_variant", "specialized"), (int(x.value) for x in v)))
+
+
+def bf_or_fold(dst, srcs, nsrc: int, src_stride_bytes: int, nbytes: int, stream=None) -> None:
+    _check(_lib.bf_or_fold(_ptr(dst), _ptr(srcs), nsrc, src_stride_bytes, nbytes, _stream(stream)))
+
+
+def bf_keygen(out, n: int | None = None, base_index: int = 0, stream=None) -> None:
+    n = out.numel() if n is None else n
+    _check(_lib.bf_keygen(_ptr(out), n, base_index, _stream(stream)))
+
+
+def bf_probe_read(buf, b: int, block_bits: int, keys, out_bits, n: int | None = None, stream=None) -> None:
+    n = keys.numel() if n is None else n
+    _check(_lib.bf_probe_read(_ptr(buf), b, block_bits, _ptr(keys), n, _ptr(out_bits), _stream(stream)))
+
+
+def bf_probe_red(buf, b: int, block_bits: int, lanes: int, keys, n: int | None = None, stream=None) -> None:
+    n = keys.numel() if n is None else n
+    _check(_lib.bf_probe_red(_ptr(buf), b, block_bits, lanes, _ptr(keys), n, _stream(stream)))
+
+
+def bf_launch_count() -> int:
+    return int(_lib.bf_launch_count())
+
+
+def bf_version() -> str:
+    return _lib.bf_version().decode()
+
+
+# ---------------------------------------------------------------- convenience
+class Filter:
+    """RAII wrapper: a device-resident Bloom filter (one bf_filter handle).
+
+    ``variant`` is "BBF" | "RBBF" | "SBF" | "CSBF" (``z`` groups for CSBF).
+    """
+
+    def __init__(self, m_bits: int, k: int, block_bits: int = 256, word_bits: int = 64,
+                 variant: str | int = "SBF", z: int = 0, seed: int = 0):
+        v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+        if v == BF_CSBF and z:
+            v = BF_CSBF_Z(z)
+        self.m_bits, self.k, self.B, self.S = m_bits, k, block_bits, word_bits
+        self.variant, self.z, self.seed = v & 0xFF, z, seed
+        self.handle = bf_create(m_bits, k, block_bits, word_bits, v, seed)
+        self.b, self.s, self.m_eff = bf_geometry(self.handle)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            bf_destroy(h)
+            self.handle = None
+
+    def add(self, keys, stream=None):
+        bf_add(self.handle, keys, keys.numel(), stream)
+
+    def contains(self, keys, out=None, stream=None):
+        import torch
+        n = keys.numel()
+        if out is None:
+            out = torch.empty((n + 31) // 32, dtype=torch.int32, device=keys.device)
+        bf_contains(self.handle, keys, out, n, stream)
+        return out
+
+    def add_host(self, host_keys, stream=None):
+        bf_add_host(self.handle, host_keys, host_keys.numel(), stream)
+
+    def contains_host(self, host_keys, out=None, stream=None):
+        import torch
+        n = host_keys.numel()
+        if out is None:
+            out = torch.empty((n + 31) // 32, dtype=torch.int32, pin_memory=True)
+        bf_contains_host(self.handle, host_keys, out, n, stream)
+        return out
+
+    def clear(self, stream=None):
+        bf_clear(self.handle, stream)
+
+    def set_layout(self, op: int, theta: int, phi: int, kpt: int = 1, hash_variant: int = 0):
+        bf_set_layout(self.handle, op, theta, phi, kpt, hash_variant)
+
+    def layout(self, op: int) -> dict:
+        return bf_get_layout(self.handle, op)
+
+    def data(self):
+        """The word array as a uint8 CUDA tensor VIEW (no copy)."""
+        import torch
+        ptr, nbytes = bf_data(self.handle)
+        return _device_view(ptr, nbytes)
+
+    def nbytes(self) -> int:
+        return bf_data(self.handle)[1]
+
+
+def _device_view(ptr: int, nbytes: int):
+    """A torch uint8 tensor aliasing `nbytes` of device memory at `ptr`."""
+    import torch
+
+    class _CAI:
+        def __init__(self, p, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (p, False),
+                                             "version": 3, "strides": None}
+    return torch.as_tensor(_CAI(ptr, nbytes), device="cuda")

@@ -1,0 +1,511 @@
+// bf_api.cu -- the C ABI of include/bf.h: validation, allocation, schedule
+// selection and launch.  Host code only; kernels live in bf_kernels.cuh
+// (specialized, instantiated in gen/inst_*.cu) and bf_util.cu.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "../../include/bf.h"
+#include "bf_internal.h"
+#include "bf_kernels.cuh"
+
+#define BF_VERSION "bf200 1.0 (sm_100a)"
+
+namespace bf {
+
+// ------------------------------------------------------------ registry
+static std::unordered_map<uint64_t, KernelFn>& registry()
+{
+    static std::unordered_map<uint64_t, KernelFn> m;
+    return m;
+}
+static std::mutex& registry_mu()
+{
+    static std::mutex mu;
+    return mu;
+}
+void registry_add(const InstKey& key, KernelFn fn)
+{
+    std::lock_guard<std::mutex> g(registry_mu());
+    registry()[key.pack()] = fn;
+}
+KernelFn registry_find(const InstKey& key)
+{
+    std::lock_guard<std::mutex> g(registry_mu());
+    auto it = registry().find(key.pack());
+    return it == registry().end() ? nullptr : it->second;
+}
+uint64_t registry_size()
+{
+    std::lock_guard<std::mutex> g(registry_mu());
+    return registry().size();
+}
+
+// ------------------------------------------------------------ errors
+static thread_local int t_code = BF_OK;
+static thread_local char t_msg[512] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+static int fail(int code, const char* fmt, ...)
+{
+    t_code = code;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(t_msg, sizeof t_msg, fmt, ap);
+    va_end(ap);
+    return code;
+}
+static int cuda_fail(cudaError_t e, const char* what)
+{
+    return fail(BF_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+static int check_launch(const char* what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return BF_OK;
+}
+
+// device guard: run on the filter's device, restore the caller's afterwards
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard()
+    {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+static int sm_count(int dev)
+{
+    static int cache[64] = {0};
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cache[dev]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        cache[dev] = v;
+    }
+    return cache[dev];
+}
+
+static bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+}  // namespace bf
+
+using namespace bf;
+
+// ------------------------------------------------------------ filter object
+struct Sched {
+    int theta, phi, kpt, hv;
+    KernelFn fn;        // specialized kernel or generic
+    bool specialized;
+    int grid;           // CTAs (persistent grid-stride)
+};
+
+struct bf_filter {
+    int device;
+    uint32_t variant, z, k, B, S, s;
+    uint64_t m_bits, b, bytes, seed;
+    void* words;
+    Sched sched[2];  // [0] add, [1] contains
+    // host-path staging (lazily allocated)
+    uint64_t* stage_keys[2];
+    uint32_t* stage_out[2];
+    uint64_t stage_n;
+    cudaStream_t copy_stream;
+    cudaEvent_t ev_ready[2], ev_free[2];
+};
+
+static int validate(uint64_t m_bits, uint32_t k, uint32_t B, uint32_t S, uint32_t variant, uint32_t* z_out)
+{
+    const uint32_t v = variant & 0xFF, z = (variant >> 8) & 0xFF;
+    if (v == BF_CBF) return fail(BF_EUNSUPPORTED, "BF_CBF is oracle-only (no GPU kernel in this build)");
+    if (v != BF_BBF && v != BF_RBBF && v != BF_SBF && v != BF_CSBF) return fail(BF_EINVAL, "unknown variant %u", v);
+    if (variant >> 16) return fail(BF_EINVAL, "unknown variant bits 0x%x", variant);
+    if (S != 32 && S != 64) return fail(BF_EINVAL, "word_bits must be 32 or 64 (got %u)", S);
+    if (!is_pow2(B) || B < S || B > 1024) return fail(BF_EINVAL, "block_bits must be a power of two in [S, 1024] (got %u)", B);
+    if (k < 1 || k > 32) return fail(BF_EINVAL, "k must be in 1..32 (got %u)", k);
+    if (m_bits < 1) return fail(BF_EINVAL, "m_bits must be >= 1");
+    const uint32_t s = B / S;
+    const uint64_t b = (m_bits + B - 1) / B;
+    if (b > (1ULL << 32)) return fail(BF_EINVAL, "too many blocks (b = %llu > 2^32)", (unsigned long long)b);
+    if (v == BF_RBBF && B != S) return fail(BF_EINVAL, "RBBF requires block_bits == word_bits");
+    if (v == BF_SBF && k % s) return fail(BF_EINVAL, "SBF requires k %% s == 0 (k=%u, s=%u)", k, s);
+    if (v == BF_CSBF) {
+        if (z < 1 || z > 16 || s % z || k % z) return fail(BF_EINVAL, "CSBF requires z | s, z | k, z <= 16 (z=%u s=%u k=%u)", z, s, k);
+    } else if (z) {
+        return fail(BF_EINVAL, "group count only valid for CSBF");
+    }
+    *z_out = (v == BF_CSBF) ? z : 0;
+    return BF_OK;
+}
+
+static int pick_grid(bf_filter* f, KernelFn fn)
+{
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, 256, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 4;
+    return per_sm * sm_count(f->device);
+}
+
+static int set_sched(bf_filter* f, int op, int theta, int phi, int kpt, int hv)
+{
+    const int s = (int)f->s;
+    if (theta == 0) {  // defaults
+        if (op == 0) { theta = s; phi = 1; }
+        else { theta = 1; phi = s; }
+        kpt = (op == 0) ? 1 : 4;
+        hv = 0;
+    }
+    if (!is_pow2(theta) || !is_pow2(phi) || theta * phi > s || theta > 32)
+        return fail(BF_EINVAL, "invalid layout Θ=%d Φ=%d for s=%d (need powers of two, Θ·Φ <= s)", theta, phi, s);
+    if (kpt != 1 && kpt != 2 && kpt != 4) return fail(BF_EINVAL, "kpt must be 1, 2 or 4");
+    if (hv < 0 || hv > 3) return fail(BF_EINVAL, "hash_variant must be 0..3");
+    InstKey key{(uint8_t)op, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z,
+                (uint8_t)theta, (uint8_t)phi, (uint8_t)kpt, (uint8_t)hv};
+    KernelFn fn = registry_find(key);
+    Sched sc{theta, phi, kpt, hv, fn, fn != nullptr, 0};
+    if (!fn) {
+        // no specialized instantiation (bf_set_layout refuses explicit
+        // requests for uncompiled schedules before getting here): the
+        // generic runtime-parameter kernel, Θ = 1, one key per thread
+        sc = Sched{1, 1, 1, 0, generic_entry((int)f->S, op == 0), false, 0};
+    }
+    sc.grid = pick_grid(f, sc.fn);
+    f->sched[op] = sc;
+    return BF_OK;
+}
+
+extern "C" {
+
+const char* bf_version(void) { return BF_VERSION; }
+
+const char* bf_last_error(int* code)
+{
+    if (code) *code = t_code;
+    return t_msg;
+}
+
+uint64_t bf_launch_count(void) { return g_launches.load(); }
+
+bf_filter* bf_create_seeded(uint64_t m_bits, uint32_t k, uint32_t block_bits, uint32_t word_bits, uint32_t variant,
+                            uint64_t seed)
+{
+    uint32_t z = 0;
+    if (validate(m_bits, k, block_bits, word_bits, variant, &z) != BF_OK) return nullptr;
+    bf_filter* f = new (std::nothrow) bf_filter();
+    if (!f) {
+        fail(BF_ENOMEM, "host allocation failed");
+        return nullptr;
+    }
+    if (cudaGetDevice(&f->device) != cudaSuccess) {
+        delete f;
+        fail(BF_ECUDA, "no CUDA device");
+        return nullptr;
+    }
+    f->variant = variant & 0xFF;
+    f->z = z;
+    f->k = k;
+    f->B = block_bits;
+    f->S = word_bits;
+    f->s = block_bits / word_bits;
+    f->m_bits = m_bits;
+    f->b = (m_bits + block_bits - 1) / block_bits;
+    f->bytes = f->b * block_bits / 8;
+    f->seed = seed;
+    cudaError_t e = cudaMalloc(&f->words, f->bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        delete f;
+        fail(BF_ENOMEM, "cudaMalloc(%llu bytes): %s", (unsigned long long)f->bytes, cudaGetErrorString(e));
+        return nullptr;
+    }
+    e = cudaMemset(f->words, 0, f->bytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(f->words);
+        delete f;
+        cuda_fail(e, "cudaMemset");
+        return nullptr;
+    }
+    if (set_sched(f, 0, 0, 0, 0, 0) != BF_OK || set_sched(f, 1, 0, 0, 0, 0) != BF_OK) {
+        cudaFree(f->words);
+        delete f;
+        return nullptr;
+    }
+    t_code = BF_OK;
+    t_msg[0] = 0;
+    return f;
+}
+
+bf_filter* bf_create(uint64_t m_bits, uint32_t k, uint32_t block_bits, uint32_t word_bits, uint32_t variant)
+{
+    return bf_create_seeded(m_bits, k, block_bits, word_bits, variant, 0);
+}
+
+static void free_staging(bf_filter* f)
+{
+    for (int i = 0; i < 2; ++i) {
+        if (f->stage_keys[i]) cudaFree(f->stage_keys[i]);
+        if (f->stage_out[i]) cudaFree(f->stage_out[i]);
+        if (f->ev_ready[i]) cudaEventDestroy(f->ev_ready[i]);
+        if (f->ev_free[i]) cudaEventDestroy(f->ev_free[i]);
+        f->stage_keys[i] = nullptr;
+        f->stage_out[i] = nullptr;
+        f->ev_ready[i] = f->ev_free[i] = nullptr;
+    }
+    if (f->copy_stream) cudaStreamDestroy(f->copy_stream);
+    f->copy_stream = nullptr;
+    f->stage_n = 0;
+}
+
+void bf_destroy(bf_filter* f)
+{
+    if (!f) return;
+    DeviceGuard g(f->device);
+    free_staging(f);
+    cudaFree(f->words);
+    delete f;
+}
+
+int bf_data(const bf_filter* f, void** dev_words, uint64_t* bytes)
+{
+    if (!f) return fail(BF_EINVAL, "null filter");
+    if (dev_words) *dev_words = f->words;
+    if (bytes) *bytes = f->bytes;
+    return BF_OK;
+}
+
+int bf_geometry(const bf_filter* f, uint64_t* b, uint32_t* s, uint64_t* m_eff_bits)
+{
+    if (!f) return fail(BF_EINVAL, "null filter");
+    if (b) *b = f->b;
+    if (s) *s = f->s;
+    if (m_eff_bits) *m_eff_bits = f->b * f->B;
+    return BF_OK;
+}
+
+int bf_set_layout(bf_filter* f, int op, int theta, int phi, int kpt, int hash_variant)
+{
+    if (!f || (op != 0 && op != 1)) return fail(BF_EINVAL, "bad filter or op");
+    DeviceGuard g(f->device);
+    if (theta == 0) return set_sched(f, op, 0, 0, 0, 0);
+    if (!is_pow2(theta) || !is_pow2(phi) || theta * phi > (int)f->s)
+        return fail(BF_EINVAL, "invalid layout Θ=%d Φ=%d for s=%u (P:L198: 1 <= Θ·Φ <= s, powers of two)", theta, phi, f->s);
+    if (kpt != 1 && kpt != 2 && kpt != 4) return fail(BF_EINVAL, "kpt must be 1, 2 or 4");
+    if (hash_variant < 0 || hash_variant > 3) return fail(BF_EINVAL, "hash_variant must be 0..3");
+    InstKey key{(uint8_t)op, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z,
+                (uint8_t)theta, (uint8_t)phi, (uint8_t)kpt, (uint8_t)hash_variant};
+    if (!registry_find(key))
+        return fail(BF_EUNSUPPORTED, "schedule Θ=%d Φ=%d kpt=%d hv=%d not compiled for this configuration", theta,
+                    phi, kpt, hash_variant);
+    return set_sched(f, op, theta, phi, kpt, hash_variant);
+}
+
+int bf_get_layout(const bf_filter* f, int op, int* theta, int* phi, int* kpt, int* hash_variant, int* specialized)
+{
+    if (!f || (op != 0 && op != 1)) return fail(BF_EINVAL, "bad filter or op");
+    const Sched& s = f->sched[op];
+    if (theta) *theta = s.theta;
+    if (phi) *phi = s.phi;
+    if (kpt) *kpt = s.kpt;
+    if (hash_variant) *hash_variant = s.hv;
+    if (specialized) *specialized = s.specialized;
+    return BF_OK;
+}
+
+static Params make_params(const bf_filter* f, const uint64_t* keys, uint64_t n, uint32_t* out)
+{
+    Params p;
+    p.words = f->words;
+    p.b = f->b;
+    p.keys = keys;
+    p.n = n;
+    p.out = out;
+    p.seed = f->seed;
+    p.variant = f->variant;
+    p.B = f->B;
+    p.S = f->S;
+    p.k = f->k;
+    p.z = f->z;
+    return p;
+}
+
+static int launch_bulk(const bf_filter* f, int op, const uint64_t* keys, uint64_t n, uint32_t* out, cudaStream_t st)
+{
+    const Sched& sc = f->sched[op];
+    const uint64_t tile_keys = sc.specialized ? 32ULL * sc.kpt : 32ULL;
+    const uint64_t tiles = (n + tile_keys - 1) / tile_keys;
+    uint64_t grid = (tiles + 7) / 8;  // 8 warps per CTA
+    if (grid > (uint64_t)sc.grid) grid = sc.grid;
+    if (grid < 1) grid = 1;
+    Params p = make_params(f, keys, n, out);
+    void* args[] = {&p};
+    cudaError_t e = cudaLaunchKernel((const void*)sc.fn, dim3((unsigned)grid), dim3(256), args, 0, st);
+    if (e != cudaSuccess) return cuda_fail(e, op ? "contains launch" : "add launch");
+    return check_launch(op ? "contains launch" : "add launch");
+}
+
+int bf_add(bf_filter* f, const uint64_t* keys, uint64_t n, void* stream)
+{
+    if (!f) return fail(BF_EINVAL, "null filter");
+    if (n == 0) return BF_OK;
+    if (!keys || ((uintptr_t)keys & 7)) return fail(BF_EINVAL, "keys must be a non-null 8-byte-aligned device pointer");
+    DeviceGuard g(f->device);
+    return launch_bulk(f, 0, keys, n, nullptr, (cudaStream_t)stream);
+}
+
+int bf_contains(const bf_filter* f, const uint64_t* keys, uint64_t n, uint32_t* out_bits, void* stream)
+{
+    if (!f) return fail(BF_EINVAL, "null filter");
+    if (n == 0) return BF_OK;
+    if (!keys || ((uintptr_t)keys & 7)) return fail(BF_EINVAL, "keys must be a non-null 8-byte-aligned device pointer");
+    if (!out_bits || ((uintptr_t)out_bits & 3)) return fail(BF_EINVAL, "out_bits must be a non-null 4-byte-aligned device pointer");
+    DeviceGuard g(f->device);
+    return launch_bulk(f, 1, keys, n, out_bits, (cudaStream_t)stream);
+}
+
+int bf_clear(bf_filter* f, void* stream)
+{
+    if (!f) return fail(BF_EINVAL, "null filter");
+    DeviceGuard g(f->device);
+    cudaError_t e = cudaMemsetAsync(f->words, 0, f->bytes, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+    return BF_OK;
+}
+
+// ------------------------------------------------------------ host path
+// Chunked, double-buffered: chunk i's host->device copy runs on an internal
+// copy stream while chunk i-1's kernel runs on the caller's stream.
+static const uint64_t kStageKeys = 1ULL << 23;  // 64 MiB of keys per buffer
+
+static int ensure_staging(bf_filter* f)
+{
+    if (f->stage_n) return BF_OK;
+    cudaError_t e = cudaStreamCreateWithFlags(&f->copy_stream, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaMalloc(&f->stage_keys[i], kStageKeys * 8);
+        if (e == cudaSuccess) e = cudaMalloc(&f->stage_out[i], kStageKeys / 8);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_ready[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_free[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+        free_staging(f);
+        cudaGetLastError();
+        return fail(BF_ENOMEM, "staging allocation: %s", cudaGetErrorString(e));
+    }
+    f->stage_n = kStageKeys;
+    return BF_OK;
+}
+
+static int host_bulk(bf_filter* f, int op, const uint64_t* hkeys, uint64_t n, uint32_t* hout, cudaStream_t st)
+{
+    int rc = ensure_staging(f);
+    if (rc) return rc;
+    cudaError_t e = cudaSuccess;
+    const uint64_t C = f->stage_n;
+    uint64_t i = 0;
+    for (uint64_t off = 0; off < n; off += C, ++i) {
+        const int buf = (int)(i & 1);
+        const uint64_t cnt = (n - off < C) ? n - off : C;
+        // copy stream: wait until the kernel that last used this buffer is done
+        if ((e = cudaStreamWaitEvent(f->copy_stream, f->ev_free[buf], 0)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(f->stage_keys[buf], hkeys + off, cnt * 8, cudaMemcpyHostToDevice,
+                                 f->copy_stream)) != cudaSuccess)
+            break;
+        if ((e = cudaEventRecord(f->ev_ready[buf], f->copy_stream)) != cudaSuccess) break;
+        if ((e = cudaStreamWaitEvent(st, f->ev_ready[buf], 0)) != cudaSuccess) break;
+        rc = launch_bulk(f, op, f->stage_keys[buf], cnt, op ? f->stage_out[buf] : nullptr, st);
+        if (rc) return rc;
+        if (op) {  // C is a multiple of 32, so chunk results are whole words
+            if ((e = cudaMemcpyAsync(hout + off / 32, f->stage_out[buf], ((cnt + 31) / 32) * 4,
+                                     cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+                break;
+        }
+        if ((e = cudaEventRecord(f->ev_free[buf], st)) != cudaSuccess) break;
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "host-buffer bulk path");
+    return BF_OK;
+}
+
+int bf_add_host(bf_filter* f, const uint64_t* host_keys, uint64_t n, void* stream)
+{
+    if (!f) return fail(BF_EINVAL, "null filter");
+    if (n == 0) return BF_OK;
+    if (!host_keys) return fail(BF_EINVAL, "null host keys");
+    DeviceGuard g(f->device);
+    return host_bulk(f, 0, host_keys, n, nullptr, (cudaStream_t)stream);
+}
+
+int bf_contains_host(const bf_filter* f, const uint64_t* host_keys, uint64_t n, uint32_t* host_out_bits, void* stream)
+{
+    if (!f) return fail(BF_EINVAL, "null filter");
+    if (n == 0) return BF_OK;
+    if (!host_keys || !host_out_bits) return fail(BF_EINVAL, "null host buffer");
+    DeviceGuard g(f->device);
+    return host_bulk((bf_filter*)f, 1, host_keys, n, host_out_bits, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------ utilities
+int bf_or_fold(void* dst, const void* srcs, uint32_t nsrc, uint64_t src_stride_bytes, uint64_t bytes, void* stream)
+{
+    if (bytes == 0) return BF_OK;
+    if (!dst || !srcs || nsrc < 1 || (bytes & 7) || (src_stride_bytes & 7) || (nsrc > 1 && src_stride_bytes < bytes))
+        return fail(BF_EINVAL, "bf_or_fold: bad arguments");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    launch_or_fold(dst, srcs, nsrc, src_stride_bytes, bytes, (cudaStream_t)stream, 4 * sm_count(dev));
+    return check_launch("or_fold launch");
+}
+
+int bf_keygen(uint64_t* out, uint64_t n, uint64_t base_index, void* stream)
+{
+    if (n == 0) return BF_OK;
+    if (!out || ((uintptr_t)out & 7)) return fail(BF_EINVAL, "bf_keygen: bad output pointer");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    launch_keygen(out, n, base_index, (cudaStream_t)stream, 8 * sm_count(dev));
+    return check_launch("keygen launch");
+}
+
+int bf_probe_read(const void* buf, uint64_t b, uint32_t block_bits, const uint64_t* keys, uint64_t n,
+                  uint32_t* out_bits, void* stream)
+{
+    if (n == 0) return BF_OK;
+    if (!buf || !keys || !out_bits || b < 1 || b > (1ULL << 32) || ((uintptr_t)keys & 7))
+        return fail(BF_EINVAL, "bf_probe_read: bad arguments");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (launch_probe_read(buf, b, block_bits, keys, n, out_bits, (cudaStream_t)stream, 8 * sm_count(dev)))
+        return fail(BF_EINVAL, "bf_probe_read: block_bits must be 64..1024");
+    return check_launch("probe_read launch");
+}
+
+int bf_probe_red(void* buf, uint64_t b, uint32_t block_bits, uint32_t lanes, const uint64_t* keys, uint64_t n,
+                 void* stream)
+{
+    if (n == 0) return BF_OK;
+    if (!buf || !keys || b < 1 || b > (1ULL << 32) || block_bits < 64 || block_bits > 1024 || !is_pow2(block_bits) ||
+        !is_pow2(lanes) || lanes > block_bits / 64)
+        return fail(BF_EINVAL, "bf_probe_red: bad arguments");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    launch_probe_red(buf, b, block_bits, lanes, keys, n, (cudaStream_t)stream, 8 * sm_count(dev));
+    return check_launch("probe_red launch");
+}
+
+}  // extern "C"

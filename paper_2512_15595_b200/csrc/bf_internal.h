@@ -1,0 +1,43 @@
+// bf_internal.h -- host-side glue shared by the library's translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bf {
+
+struct Params;
+typedef void (*KernelFn)(Params);
+
+// Key of a specialized kernel instantiation.
+struct InstKey {
+    uint8_t op;       // 0 add, 1 contains
+    uint8_t variant;  // BF_BBF..BF_CSBF
+    uint16_t B;
+    uint8_t S, k, z, theta, phi, kpt, hv;
+    uint64_t pack() const
+    {
+        return (uint64_t)op | ((uint64_t)variant << 2) | ((uint64_t)(B / 32) << 5) | ((uint64_t)(S == 64) << 11) |
+               ((uint64_t)k << 12) | ((uint64_t)z << 18) | ((uint64_t)theta << 24) | ((uint64_t)phi << 30) |
+               ((uint64_t)kpt << 36) | ((uint64_t)hv << 40);
+    }
+};
+
+void registry_add(const InstKey& key, KernelFn fn);
+KernelFn registry_find(const InstKey& key);
+uint64_t registry_size();
+
+KernelFn generic_entry(int S, bool add);
+void launch_keygen(uint64_t* out, uint64_t n, uint64_t base, cudaStream_t st, int grid);
+void launch_or_fold(void* dst, const void* srcs, uint32_t nsrc, uint64_t stride, uint64_t bytes,
+                    cudaStream_t st, int grid);
+int launch_probe_read(const void* buf, uint64_t b, uint32_t B, const uint64_t* keys, uint64_t n,
+                      uint32_t* out, cudaStream_t st, int grid);
+void launch_probe_red(void* buf, uint64_t b, uint32_t B, uint32_t lanes, const uint64_t* keys, uint64_t n,
+                      cudaStream_t st, int grid);
+
+struct Registrar {
+    Registrar(void (*fn)()) { fn(); }
+};
+
+}  // namespace bf

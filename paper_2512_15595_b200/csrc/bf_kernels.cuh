@@ -1,0 +1,416 @@
+// bf_kernels.cuh -- bulk add / contains kernels for sm_100a (arXiv 2512.15595).
+//
+// One warp owns a tile of 32*KPT consecutive keys (P:L245 step (1): "A warp is
+// assigned a contiguous chunk of ... consecutive input keys ... Each thread
+// computes the hash value of its key").  Lane l loads keys l*KPT .. l*KPT+KPT-1
+// of the tile with ONE 128/256-bit load (coalesced: the warp reads 256*KPT
+// contiguous bytes) and hashes them once.
+//
+// Θ == 1 (the contains default, "Θ=1 and Φ=s for B<=256"): each lane
+// handles its own keys; the whole block is fetched with s/Φ loads of Φ words
+// (one LDG.256 for a 256-bit block) and AND-compared in registers.
+//
+// Θ > 1 (the add default Θ = s, "a fully horizontal layout ... Θ̂_a =
+// s"): groups of Θ lanes take turns broadcasting (block, lo) of one key with
+// two register shuffles (P:L245 step (2)); every lane of the group builds the
+// masks of its own words (st*Θ*Φ + pos*Φ + φ, Fig. 2) and issues its
+// red.global.or / loads in the same instruction, so L1 coalesces the group
+// into one L2 request per sector.  contains combines the
+// group's verdict with one ballot.
+//
+// Results (contains) stay in registers until the tile is done, then one
+// ballot per key slot packs them and KPT lanes store KPT consecutive words
+// (P:L245 step (3) "written back in a coalesced fashion").
+//
+// The salts are compile-time immediates whenever the word index is
+// compile-time (Θ = 1), per-thread registers loaded once per kernel when the
+// word index depends on the lane (Θ > 1) -- this replaces the paper's
+// compile-time decision tree over salt indices: a lane's
+// position in its group never changes, so its salts never change either.
+// hash_variant 1/2/3 are the ablations of P:L228-243 (constant-bank table,
+// shared-memory table, per-lane re-hashing), all bit-identical.
+#pragma once
+
+#include "bf_device.cuh"
+
+namespace bf {
+
+struct Params {
+    void* words;           // filter word array (b * s words of S bits)
+    uint64_t b;            // number of blocks
+    const uint64_t* keys;  // device keys
+    uint64_t n;            // number of keys
+    uint32_t* out;         // contains: ceil(n/32) result words
+    uint64_t seed;         // XXH64 seed
+    // runtime geometry (generic kernel only)
+    uint32_t variant, B, S, k, z;
+};
+
+template <int V_, int S_, int LGS_, int K_, int Z_, int THETA_, int PHI_, int KPT_, int HV_>
+struct Cfg {
+    static constexpr int V = V_, S = S_, s = 1 << LGS_, K = K_;
+    static constexpr int Z = (V_ == V_CSBF) ? Z_ : 1;
+    static constexpr int THETA = THETA_, PHI = PHI_, KPT = KPT_, HV = HV_;
+    static constexpr int B = S * s, LGB = ilog2(B), LGW = ilog2(S);
+    static constexpr int G = (V == V_CSBF) ? s / Z : 1, LGG = ilog2(G);
+    static constexpr int Q = (V == V_SBF || V == V_RBBF) ? K / s : (V == V_CSBF ? K / Z : K);
+    static constexpr int STEPS = s / (THETA * PHI);
+    static constexpr int NSLOT = STEPS * PHI;  // words per lane
+    using W = typename WordT<S>::T;
+
+    static_assert(S == 32 || S == 64, "word size");
+    static_assert(THETA >= 1 && THETA <= 32 && (THETA & (THETA - 1)) == 0, "Θ power of two");
+    static_assert(PHI >= 1 && (PHI & (PHI - 1)) == 0, "Φ power of two");
+    static_assert(THETA * PHI <= s, "1 <= Θ·Φ <= s (P:L198)");
+    static_assert(K >= 1 && K <= 32, "k");
+    static_assert(V != V_SBF || K % s == 0, "SBF needs k % s == 0");
+    static_assert(V != V_RBBF || s == 1, "RBBF needs B == S");
+    static_assert(V != V_CSBF || (s % Z == 0 && K % Z == 0), "CSBF needs z | s, z | k");
+    static_assert(KPT == 1 || KPT == 2 || KPT == 4, "keys per thread");
+    static_assert(HV >= 0 && HV <= 3, "hash variant");
+
+    // word of slot `slot` for the lane at position `pos` of its group
+    static __device__ __forceinline__ uint32_t word(int slot, uint32_t pos)
+    {
+        const int st = slot / PHI, ph = slot % PHI;
+        return (uint32_t)(st * THETA * PHI + ph) + pos * PHI;
+    }
+    // index of draw t of word w (SBF / CSBF)
+    static __host__ __device__ __forceinline__ uint32_t draw(uint32_t w, int t)
+    {
+        if constexpr (V == V_CSBF) return (w >> LGG) * Q + t;
+        else return w * Q + t;
+    }
+};
+
+// ----------------------------------------------------------------- salts
+template <class C> struct SaltSrc {
+    static constexpr bool kRegs = (C::THETA > 1) && (C::HV == 0 || C::HV == 3) && C::V != V_BBF;
+    static constexpr int NR = kRegs ? C::NSLOT : 1;
+    static constexpr int QR = kRegs ? C::Q : 1;
+    uint32_t r[NR][QR];
+    uint32_t g[NR];
+    const uint32_t* sm;
+    const uint32_t* gsm;
+
+    __device__ __forceinline__ void init(uint32_t pos, const uint32_t* smem_salt, const uint32_t* smem_gsalt)
+    {
+        sm = smem_salt;
+        gsm = smem_gsalt;
+        if constexpr (kRegs) {
+#pragma unroll
+            for (int slot = 0; slot < C::NSLOT; ++slot) {
+                const uint32_t w = C::word(slot, pos);
+#pragma unroll
+                for (int t = 0; t < C::Q; ++t) r[slot][t] = c_salt[C::draw(w, t)];
+                if constexpr (C::V == V_CSBF) g[slot] = c_gsalt[w >> C::LGG];
+            }
+        }
+    }
+
+    // salt of draw T of slot SLOT whose word is w (w == SLOT when Θ == 1)
+    template <int SLOT, int T> __device__ __forceinline__ uint32_t salt(uint32_t w) const
+    {
+        if constexpr (C::HV == 1) return c_salt[C::draw(w, T)];
+        else if constexpr (C::HV == 2) return sm[C::draw(w, T)];
+        else if constexpr (kRegs) return r[SLOT][T];
+        else return salt_ct((int)C::draw((uint32_t)SLOT, T));
+    }
+    template <int SLOT> __device__ __forceinline__ uint32_t gsalt(uint32_t w) const
+    {
+        if constexpr (C::HV == 1) return c_gsalt[w >> C::LGG];
+        else if constexpr (C::HV == 2) return gsm[w >> C::LGG];
+        else if constexpr (kRegs) return g[SLOT];
+        else return gsalt_ct(SLOT >> C::LGG);
+    }
+    template <int J> __device__ __forceinline__ uint32_t bbf_salt() const
+    {
+        if constexpr (C::HV == 1) return c_salt[J];
+        else if constexpr (C::HV == 2) return sm[J];
+        else return salt_ct(J);
+    }
+};
+
+// ----------------------------------------------------------------- pattern
+// Mask of word w (slot SLOT of this lane) for a key with low hash half lo,
+// DESIGN.md section 2 / P:L115-132.
+template <class C, int SLOT>
+__device__ __forceinline__ typename C::W slot_mask(uint32_t lo, uint32_t w, const SaltSrc<C>& ss)
+{
+    using W = typename C::W;
+    W m = 0;
+    if constexpr (C::V == V_SBF || C::V == V_RBBF) {
+        StaticFor<0, C::Q>::run([&](auto T) {
+            const uint32_t d = lo * ss.template salt<SLOT, decltype(T)::value>(w);
+            m |= W(1) << (d >> (32 - C::LGW));
+        });
+    } else if constexpr (C::V == V_CSBF) {
+        StaticFor<0, C::Q>::run([&](auto T) {
+            const uint32_t d = lo * ss.template salt<SLOT, decltype(T)::value>(w);
+            m |= W(1) << (d >> (32 - C::LGW));
+        });
+        if constexpr (C::G > 1) {
+            const uint32_t sel = (lo * ss.template gsalt<SLOT>(w)) >> (32 - C::LGG);
+            m = ((w & (C::G - 1)) == sel) ? m : W(0);
+        }
+    } else {  // BBF: k draws over the whole block; keep those landing in word w
+        StaticFor<0, C::K>::run([&](auto J) {
+            const uint32_t p = (lo * ss.template bbf_salt<decltype(J)::value>()) >> (32 - C::LGB);
+            m |= shl_clamp(W(1), p - w * (uint32_t)C::S);
+        });
+    }
+    return m;
+}
+
+// ----------------------------------------------------------------- per key
+// Select a[idx] from a compile-time-sized register array without local memory
+// (a SEL chain; N <= 32).
+template <int N, class W>
+__device__ __forceinline__ W pick(const W* a, uint32_t idx)
+{
+    W r = a[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) r = (idx == (uint32_t)i) ? a[i] : r;
+    return r;
+}
+
+// Load the whole block of a key (Θ == 1): s/Φ loads of Φ contiguous words.
+template <class C>
+__device__ __forceinline__ void load_block(const typename C::W* F, uint32_t blk, typename C::W* wd)
+{
+    const typename C::W* bp = F + (uint64_t)blk * C::s;
+    StaticFor<0, C::STEPS>::run([&](auto ST) {
+        VecLoad<C::S, C::PHI>::run(bp + decltype(ST)::value * C::PHI, wd + decltype(ST)::value * C::PHI);
+    });
+}
+
+// contains on a loaded block (Θ == 1).  Every draw is tested directly as a
+// bit of its word -- (word >> bit) & 1, one funnel shift for 64-bit words --
+// instead of building and comparing masks; bit 0 of the AND of all tests is
+// the answer ("If any bit is zero, the element is certainly not in the
+// set").
+template <class C>
+__device__ __forceinline__ bool test_block(const typename C::W* wd, uint32_t lo, const SaltSrc<C>& ss)
+{
+    using W = typename C::W;
+    uint32_t acc = 0xffffffffu;
+    if constexpr (C::V == V_SBF || C::V == V_RBBF) {
+        StaticFor<0, C::s>::run([&](auto I) {
+            constexpr int w = decltype(I)::value;
+            StaticFor<0, C::Q>::run([&](auto T) {
+                const uint32_t d = lo * ss.template salt<w, decltype(T)::value>((uint32_t)w);
+                acc &= (uint32_t)(wd[w] >> (d >> (32 - C::LGW)));
+            });
+        });
+    } else if constexpr (C::V == V_CSBF) {
+        StaticFor<0, C::Z>::run([&](auto I) {
+            constexpr int w0 = decltype(I)::value * C::G;  // first word of group i
+            W x;
+            if constexpr (C::G > 1) {
+                const uint32_t sel = (lo * ss.template gsalt<w0>((uint32_t)w0)) >> (32 - C::LGG);
+                x = pick<C::G>(wd + w0, sel);
+            } else {
+                x = wd[w0];
+            }
+            StaticFor<0, C::Q>::run([&](auto T) {
+                const uint32_t d = lo * ss.template salt<w0, decltype(T)::value>((uint32_t)w0);
+                acc &= (uint32_t)(x >> (d >> (32 - C::LGW)));
+            });
+        });
+    } else {  // BBF
+        StaticFor<0, C::K>::run([&](auto J) {
+            const uint32_t p = (lo * ss.template bbf_salt<decltype(J)::value>()) >> (32 - C::LGB);
+            const W x = (C::s > 1) ? pick<C::s>(wd, p >> C::LGW) : wd[0];
+            acc &= (uint32_t)(x >> (p & (C::S - 1)));
+        });
+    }
+    return acc & 1u;
+}
+
+// contains, this lane's words of a block (Θ > 1): returns the missing bits.
+template <class C>
+__device__ __forceinline__ typename C::W contains_part(const typename C::W* F, uint32_t lo, uint32_t blk,
+                                                      uint32_t pos, const SaltSrc<C>& ss)
+{
+    using W = typename C::W;
+    const W* bp = F + (uint64_t)blk * C::s + pos * C::PHI;
+    W wd[C::NSLOT];
+    StaticFor<0, C::STEPS>::run([&](auto ST) {
+        VecLoad<C::S, C::PHI>::run(bp + decltype(ST)::value * C::THETA * C::PHI, wd + decltype(ST)::value * C::PHI);
+    });
+    W acc = 0;
+    StaticFor<0, C::NSLOT>::run([&](auto SL) {
+        const W m = slot_mask<C, decltype(SL)::value>(lo, C::word(decltype(SL)::value, pos), ss);
+        acc |= m & ~wd[decltype(SL)::value];
+    });
+    return acc;
+}
+
+// add, this lane's words of a block (pos = 0 and all words when Θ == 1).
+template <class C>
+__device__ __forceinline__ void add_part(typename C::W* F, uint32_t lo, uint32_t blk, uint32_t pos,
+                                         const SaltSrc<C>& ss)
+{
+    using W = typename C::W;
+    W* bp = F + (uint64_t)blk * C::s;
+    StaticFor<0, C::NSLOT>::run([&](auto SL) {
+        const uint32_t w = (C::THETA == 1) ? (uint32_t)decltype(SL)::value : C::word(decltype(SL)::value, pos);
+        const W m = slot_mask<C, decltype(SL)::value>(lo, w, ss);
+        if constexpr (C::V == V_SBF || C::V == V_RBBF) {
+            red_or(bp + w, m);  // every SBF word receives >= 1 bit
+        } else {
+            if (m) red_or(bp + w, m);
+        }
+    });
+}
+
+// ----------------------------------------------------------------- results
+template <int KPT>
+__device__ __forceinline__ void store_results(uint32_t* out, uint64_t tile, uint32_t res, uint32_t lane,
+                                              uint64_t nwords)
+{
+    if constexpr (KPT == 1) {
+        const uint32_t b = __ballot_sync(0xffffffffu, res & 1u);
+        if (lane == 0 && tile < nwords) out[tile] = b;
+    } else if constexpr (KPT == 2) {
+        const uint32_t b0 = __ballot_sync(0xffffffffu, res & 1u);
+        const uint32_t b1 = __ballot_sync(0xffffffffu, (res >> 1) & 1u);
+        if (lane < 2) {
+            const uint64_t idx = tile * 2 + lane;
+            const uint32_t wv = spread2(b0 >> (16 * lane)) | (spread2(b1 >> (16 * lane)) << 1);
+            if (idx < nwords) out[idx] = wv;
+        }
+    } else {
+        const uint32_t b0 = __ballot_sync(0xffffffffu, res & 1u);
+        const uint32_t b1 = __ballot_sync(0xffffffffu, (res >> 1) & 1u);
+        const uint32_t b2 = __ballot_sync(0xffffffffu, (res >> 2) & 1u);
+        const uint32_t b3 = __ballot_sync(0xffffffffu, (res >> 3) & 1u);
+        if (lane < 4) {
+            const uint64_t idx = tile * 4 + lane;
+            const uint32_t sh = 8 * lane;
+            const uint32_t wv = spread4(b0 >> sh) | (spread4(b1 >> sh) << 1) | (spread4(b2 >> sh) << 2) |
+                                (spread4(b3 >> sh) << 3);
+            if (idx < nwords) out[idx] = wv;
+        }
+    }
+}
+
+// ----------------------------------------------------------------- tile
+template <class C, bool ADD, bool FULL>
+__device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_t lane, uint32_t pos,
+                                         uint32_t gbase, bool vec_ok, const SaltSrc<C>& ss)
+{
+    using W = typename C::W;
+    constexpr int KPT = C::KPT;
+    const uint64_t base = tile * (32 * KPT);
+    const uint64_t mine = base + (uint64_t)lane * KPT;
+
+    // (1) ingest + hash once per key
+    uint64_t key[KPT];
+    bool valid[KPT];
+    if (FULL && vec_ok) {
+        if constexpr (KPT == 4) ld_keys4(p.keys + mine, key);
+        else if constexpr (KPT == 2) ld_keys2(p.keys + mine, key);
+        else key[0] = ld_key1(p.keys + mine);
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) valid[j] = true;
+    } else {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            valid[j] = FULL || (mine + j < p.n);
+            key[j] = valid[j] ? ld_key1(p.keys + mine + j) : 0ULL;
+        }
+    }
+    uint32_t lo[KPT], blk[KPT];
+    if constexpr (!(C::HV == 3 && C::THETA > 1)) {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            const uint64_t h = xxh64_u64(key[j], p.seed);
+            lo[j] = (uint32_t)h;
+            blk[j] = block_of(h, p.b);
+        }
+    }
+
+    uint32_t res = 0;
+    if constexpr (C::THETA == 1 && ADD) {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j)
+            if (FULL || valid[j]) add_part<C>((W*)p.words, lo[j], blk[j], 0, ss);
+    } else if constexpr (C::THETA == 1) {
+        // issue every block load of the tile before testing any (memory-level
+        // parallelism: KPT*s/Φ loads in flight per lane)
+        W wd[KPT][C::s];
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            if (FULL || valid[j]) load_block<C>((const W*)p.words, blk[j], wd[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            if (FULL || valid[j]) res |= (uint32_t)test_block<C>(wd[j], lo[j], ss) << j;
+        }
+    } else {
+        // (2) group-cooperative execution, one key of the group at a time
+        constexpr uint32_t GMASK = (C::THETA == 32) ? 0xffffffffu : ((1u << C::THETA) - 1u);
+#pragma unroll 1
+        for (int r = 0; r < C::THETA; ++r) {
+            const uint32_t src = gbase + r;
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) {
+                uint32_t l, bk;
+                bool v;
+                if constexpr (C::HV == 3) {  // ablation: every lane re-hashes the key itself
+                    const uint64_t idx = base + (uint64_t)src * KPT + j;
+                    v = FULL || idx < p.n;
+                    const uint64_t h = xxh64_u64(v ? p.keys[idx] : 0ULL, p.seed);
+                    l = (uint32_t)h;
+                    bk = block_of(h, p.b);
+                } else {
+                    l = __shfl_sync(0xffffffffu, lo[j], src);
+                    bk = __shfl_sync(0xffffffffu, blk[j], src);
+                    v = FULL || __shfl_sync(0xffffffffu, (int)valid[j], src);
+                }
+                if constexpr (ADD) {
+                    if (v) add_part<C>((W*)p.words, l, bk, pos, ss);
+                } else {
+                    const W miss = v ? contains_part<C>((const W*)p.words, l, bk, pos, ss) : W(0);
+                    const uint32_t ball = __ballot_sync(0xffffffffu, miss != 0);
+                    const uint32_t ok = (((ball >> gbase) & GMASK) == 0) && v;
+                    if (pos == (uint32_t)r) res |= ok << j;
+                }
+            }
+        }
+    }
+
+    // (3) coalesced write-back of the packed results
+    if constexpr (!ADD) store_results<KPT>(p.out, tile, res, lane, (p.n + 31) / 32);
+}
+
+template <class C, bool ADD>
+__global__ void __launch_bounds__(256) bulk_kernel(const Params p)
+{
+    __shared__ uint32_t s_salt[C::HV == 2 ? 64 : 1];
+    __shared__ uint32_t s_gsalt[C::HV == 2 ? 16 : 1];
+    if constexpr (C::HV == 2) {
+        if (threadIdx.x < 64) s_salt[threadIdx.x] = c_salt[threadIdx.x];
+        if (threadIdx.x < 16) s_gsalt[threadIdx.x] = c_gsalt[threadIdx.x];
+        __syncthreads();
+    }
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t pos = lane & (uint32_t)(C::THETA - 1);
+    const uint32_t gbase = lane & ~(uint32_t)(C::THETA - 1);
+    SaltSrc<C> ss;
+    ss.init(pos, s_salt, s_gsalt);
+
+    constexpr uint64_t TILE = 32 * C::KPT;
+    const uint64_t ntiles = (p.n + TILE - 1) / TILE;
+    const uint64_t nfull = p.n / TILE;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const bool vec_ok = (((uintptr_t)p.keys) & (8 * C::KPT - 1)) == 0;
+    for (uint64_t t = gw; t < ntiles; t += nw) {
+        if (t < nfull) run_tile<C, ADD, true>(p, t, lane, pos, gbase, vec_ok, ss);
+        else run_tile<C, ADD, false>(p, t, lane, pos, gbase, vec_ok, ss);
+    }
+}
+
+}  // namespace bf

@@ -1,0 +1,230 @@
+// bf_util.cu -- the runtime-parameter (generic) add/contains kernels, the
+// synthetic key generator, the multi-GPU OR-fold and the roofline probes.
+#include <cuda_runtime.h>
+
+#include "bf_internal.h"
+#include "bf_kernels.cuh"
+
+namespace bf {
+
+// ------------------------------------------------------------ generic path
+// Θ = 1, one key per thread, every geometry parameter at run time and the
+// salts read from the constant bank.  Covers every valid configuration
+// (including B = 512/1024) that has no specialized instantiation; same
+// arithmetic as DESIGN.md section 2.
+template <int S>
+__device__ __forceinline__ typename WordT<S>::T generic_mask(const Params& p, uint32_t lo, uint32_t w,
+                                                            uint32_t s)
+{
+    using W = typename WordT<S>::T;
+    constexpr uint32_t LGW = (S == 32) ? 5 : 6;
+    W m = 0;
+    if (p.variant == V_BBF) {
+        const uint32_t lgB = 31 - __clz(p.B);
+        for (uint32_t j = 0; j < p.k; ++j) {
+            const uint32_t pos = (lo * c_salt[j]) >> (32 - lgB);
+            m |= shl_clamp(W(1), pos - w * (uint32_t)S);
+        }
+    } else if (p.variant == V_CSBF) {
+        const uint32_t g = s / p.z, q = p.k / p.z, grp = w / g;
+        if (g > 1) {
+            const uint32_t lgg = 31 - __clz(g);
+            const uint32_t sel = (lo * c_gsalt[grp]) >> (32 - lgg);
+            if ((w & (g - 1)) != sel) return 0;
+        }
+        for (uint32_t t = 0; t < q; ++t) m |= W(1) << ((lo * c_salt[grp * q + t]) >> (32 - LGW));
+    } else {  // SBF, RBBF
+        const uint32_t q = p.k / s;
+        for (uint32_t t = 0; t < q; ++t) m |= W(1) << ((lo * c_salt[w * q + t]) >> (32 - LGW));
+    }
+    return m;
+}
+
+template <int S, bool ADD>
+__global__ void __launch_bounds__(256) generic_kernel(const Params p)
+{
+    using W = typename WordT<S>::T;
+    const uint32_t s = p.B / S;
+    const uint64_t n32 = (p.n + 31) & ~31ULL;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n32; i += stride) {
+        const bool valid = i < p.n;
+        bool ok = false;
+        if (valid) {
+            const uint64_t h = xxh64_u64(p.keys[i], p.seed);
+            const uint32_t lo = (uint32_t)h, blk = block_of(h, p.b);
+            W* bp = (W*)p.words + (uint64_t)blk * s;
+            ok = true;
+            for (uint32_t w = 0; w < s; ++w) {
+                const W m = generic_mask<S>(p, lo, w, s);
+                if (ADD) {
+                    if (m) red_or(bp + w, m);
+                } else if ((bp[w] & m) != m) {
+                    ok = false;
+                }
+            }
+        }
+        if (!ADD) {
+            const uint32_t ball = __ballot_sync(0xffffffffu, ok);
+            if ((threadIdx.x & 31) == 0) p.out[i >> 5] = ball;
+        }
+    }
+}
+
+KernelFn generic_entry(int S, bool add)
+{
+    if (S == 32) return add ? (KernelFn)generic_kernel<32, true> : (KernelFn)generic_kernel<32, false>;
+    return add ? (KernelFn)generic_kernel<64, true> : (KernelFn)generic_kernel<64, false>;
+}
+
+// ------------------------------------------------------------ key generator
+__global__ void __launch_bounds__(256) keygen_kernel(uint64_t* out, uint64_t n, uint64_t base)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const bool vec = (((uintptr_t)out) & 15) == 0;
+    if (vec) {
+        const uint64_t n2 = n / 2;
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+            ulonglong2 v;
+            v.x = mix64(base + 2 * i);
+            v.y = mix64(base + 2 * i + 1);
+            reinterpret_cast<ulonglong2*>(out)[i] = v;
+        }
+        if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) out[n - 1] = mix64(base + n - 1);
+    } else {
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+            out[i] = mix64(base + i);
+    }
+}
+
+void launch_keygen(uint64_t* out, uint64_t n, uint64_t base, cudaStream_t st, int grid)
+{
+    keygen_kernel<<<grid, 256, 0, st>>>(out, n, base);
+}
+
+// ------------------------------------------------------------ OR-fold
+// dst[i] = OR_r src_r[i]; 16-byte vectors, streaming (HBM-bound: reads
+// nsrc*bytes, writes bytes).
+__global__ void __launch_bounds__(256) or_fold_kernel(uint4* dst, const uint4* src, uint32_t nsrc,
+                                                      uint64_t stride16, uint64_t n16)
+{
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += step) {
+        uint4 a = src[i];
+        for (uint32_t r = 1; r < nsrc; ++r) {
+            const uint4 v = src[i + r * stride16];
+            a.x |= v.x;
+            a.y |= v.y;
+            a.z |= v.z;
+            a.w |= v.w;
+        }
+        dst[i] = a;
+    }
+}
+
+__global__ void __launch_bounds__(256) or_fold_kernel8(uint64_t* dst, const uint64_t* src, uint32_t nsrc,
+                                                       uint64_t stride8, uint64_t n8)
+{
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += step) {
+        uint64_t a = src[i];
+        for (uint32_t r = 1; r < nsrc; ++r) a |= src[i + r * stride8];
+        dst[i] = a;
+    }
+}
+
+void launch_or_fold(void* dst, const void* srcs, uint32_t nsrc, uint64_t stride, uint64_t bytes,
+                    cudaStream_t st, int grid)
+{
+    const bool v16 = ((((uintptr_t)dst) | ((uintptr_t)srcs) | stride | bytes) & 15) == 0;
+    if (v16)
+        or_fold_kernel<<<grid, 256, 0, st>>>((uint4*)dst, (const uint4*)srcs, nsrc, stride / 16, bytes / 16);
+    else
+        or_fold_kernel8<<<grid, 256, 0, st>>>((uint64_t*)dst, (const uint64_t*)srcs, nsrc, stride / 8, bytes / 8);
+}
+
+// ------------------------------------------------------------ probes
+// R_read: the contains access pattern with hashing and pattern generation
+// removed: block = ((key >> 32) * b) >> 32, one wide load of the block,
+// AND-reduce, ballot-packed bit per key.  4 keys per lane like the product.
+template <int BB>
+__global__ void __launch_bounds__(256) probe_read_kernel(const unsigned long long* buf, uint64_t b,
+                                                         const uint64_t* keys, uint64_t n, uint32_t* out)
+{
+    constexpr int NW = BB / 64;  // 64-bit words per block (>= 1)
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t ntiles = (n + 127) / 128;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = gw; t < ntiles; t += nw) {
+        const uint64_t mine = t * 128 + lane * 4;
+        uint64_t k[4];
+        if (mine + 4 <= n) ld_keys4(keys + mine, k);
+        else
+            for (int j = 0; j < 4; ++j) k[j] = (mine + j < n) ? keys[mine + j] : 0;
+        uint32_t res = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t blk = ((k[j] >> 32) * b) >> 32;
+            unsigned long long w[NW < 4 ? 4 : NW];
+            if constexpr (NW == 1) VecLoad<64, 1>::run(buf + blk, w);
+            else if constexpr (NW == 2) VecLoad<64, 2>::run(buf + blk * 2, w);
+            else VecLoad<64, NW>::run(buf + blk * NW, w);
+            unsigned long long a = ~0ULL;
+#pragma unroll
+            for (int i = 0; i < NW; ++i) a &= w[i] | k[j];
+            res |= (uint32_t)(a == ~0ULL) << j;
+        }
+        store_results<4>(out, t, res, lane, (n + 31) / 32);
+    }
+}
+
+// R_red: the add access pattern without hashing: `lanes` lanes cooperate on
+// a key (one shuffle of the block index) and each issues one 64-bit
+// red.global.or into its word; lanes == 1 is the 64-bit GUPS update.
+__global__ void __launch_bounds__(256) probe_red_kernel(unsigned long long* buf, uint64_t b, uint32_t nwords,
+                                                        uint32_t lanes, const uint64_t* keys, uint64_t n)
+{
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t pos = lane & (lanes - 1), gbase = lane & ~(lanes - 1);
+    const uint64_t ntiles = (n + 31) / 32;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = gw; t < ntiles; t += nw) {
+        const uint64_t i = t * 32 + lane;
+        const uint64_t k = i < n ? ld_key1(keys + i) : 0;
+        const uint32_t blk = (uint32_t)(((k >> 32) * b) >> 32);
+        for (uint32_t r = 0; r < lanes; ++r) {
+            const uint32_t src = gbase + r;
+            const uint32_t bk = __shfl_sync(0xffffffffu, blk, src);
+            const uint64_t kk = __shfl_sync(0xffffffffu, k, src);
+            const bool v = (t * 32 + src) < n;
+            if (v)
+                for (uint32_t w = pos; w < nwords; w += lanes)
+                    red_or(buf + (uint64_t)bk * nwords + w, 1ULL << ((kk >> (6 * w)) & 63));
+        }
+    }
+}
+
+int launch_probe_read(const void* buf, uint64_t b, uint32_t B, const uint64_t* keys, uint64_t n, uint32_t* out,
+                      cudaStream_t st, int grid)
+{
+    const unsigned long long* p = (const unsigned long long*)buf;
+    switch (B) {
+    case 64: probe_read_kernel<64><<<grid, 256, 0, st>>>(p, b, keys, n, out); break;
+    case 128: probe_read_kernel<128><<<grid, 256, 0, st>>>(p, b, keys, n, out); break;
+    case 256: probe_read_kernel<256><<<grid, 256, 0, st>>>(p, b, keys, n, out); break;
+    case 512: probe_read_kernel<512><<<grid, 256, 0, st>>>(p, b, keys, n, out); break;
+    case 1024: probe_read_kernel<1024><<<grid, 256, 0, st>>>(p, b, keys, n, out); break;
+    default: return -1;
+    }
+    return 0;
+}
+
+void launch_probe_red(void* buf, uint64_t b, uint32_t B, uint32_t lanes, const uint64_t* keys, uint64_t n,
+                      cudaStream_t st, int grid)
+{
+    probe_red_kernel<<<grid, 256, 0, st>>>((unsigned long long*)buf, b, B / 64, lanes, keys, n);
+}
+
+}  // namespace bf

@@ -17,3 +17,21 @@ def pytest_configure(config):
 def oracle_lib():
     from oracle import bfo
     return bfo.lib()
+
+
+@pytest.fixture(scope="session")
+def bflib():
+    """The CUDA library (built in-tree if missing; nvcc cross-compiles here)."""
+    from paper_2512_15595_b200 import build
+    build.build()
+    from paper_2512_15595_b200 import bf
+    return bf
+
+
+@pytest.fixture(scope="session")
+def cuda(bflib):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.init()
+    return torch.device("cuda:0")

@@ -1,0 +1,69 @@
+"""The C-ABI library builds for sm_100a, loads, and exports every symbol
+include/bf.h declares (no compute calls: this runs on the CPU box)."""
+import ctypes
+import os
+import subprocess
+
+import pytest
+
+
+def test_library_exports_every_declared_symbol(bflib):
+    declared = bflib.declared_symbols()
+    assert len(declared) >= 19
+    lib = ctypes.CDLL(bflib.LIB_PATH)
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
+    out = subprocess.run(["nm", "-D", "--defined-only", bflib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {l.split()[-1] for l in out.splitlines() if " T bf_" in l}
+    assert set(declared) <= exported
+    assert bflib.bf_version().startswith("bf200")
+
+
+def test_library_is_sm100a_code(bflib):
+    out = subprocess.run(["cuobjdump", "--list-elf", bflib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_sass_has_256bit_loads_and_red_or(bflib):
+    """Codegen check: contains uses LDG.E.*.256, add uses REDG.E.OR."""
+    sass = subprocess.run(["cuobjdump", "-sass", bflib.LIB_PATH], capture_output=True, text=True).stdout
+    assert ".256" in sass and "LDG.E" in sass
+    assert "REDG.E.OR.64" in sass and "REDG.E.OR.STRONG" in sass
+
+
+def test_validation_without_gpu(bflib):
+    """Invalid configurations are rejected synchronously (BF_EINVAL) before any
+    CUDA call; CBF is BF_EUNSUPPORTED."""
+    bf = bflib
+    with pytest.raises(bf.BFError) as e:
+        bf.bf_create(1 << 20, 10, 256, 64, bf.BF_SBF)  # k % s != 0
+    assert e.value.code == bf.BF_EINVAL
+    with pytest.raises(bf.BFError) as e:
+        bf.bf_create(1 << 20, 8, 128, 64, bf.BF_RBBF)
+    assert e.value.code == bf.BF_EINVAL
+    with pytest.raises(bf.BFError) as e:
+        bf.bf_create(1 << 20, 8, 256, 48, bf.BF_BBF)
+    assert e.value.code == bf.BF_EINVAL
+    with pytest.raises(bf.BFError) as e:
+        bf.bf_create(1 << 20, 6, 256, 32, bf.BF_CSBF_Z(4))  # k % z != 0
+    assert e.value.code == bf.BF_EINVAL
+    with pytest.raises(bf.BFError) as e:
+        bf.bf_create(1 << 20, 8, 256, 64, bf.BF_CBF)
+    assert e.value.code == bf.BF_EUNSUPPORTED
+    with pytest.raises(bf.BFError) as e:
+        bf.bf_create(1 << 20, 0, 256, 64, bf.BF_BBF)
+    assert e.value.code == bf.BF_EINVAL
+
+
+def test_instantiation_table_matches_generator(bflib):
+    import importlib.util
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location(
+        "gen_instances", os.path.join(here, "paper_2512_15595_b200", "csrc", "gen_instances.py"))
+    g = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(g)
+    inst = g.instances()
+    assert len(inst) > 500
+    # every configs[1] sweep row has both default layouts compiled
+    assert (1, 3, 256, 64, 8, 0, 1, 4, 4, 0) in inst  # contains SBF 256/64 k8 Θ1 Φ4 kpt4
+    assert (0, 3, 256, 64, 8, 0, 4, 1, 1, 0) in inst  # add SBF 256/64 k8 Θ4 Φ1

@@ -1,0 +1,340 @@
+"""GPU parity: the CUDA path (through the C ABI) reproduces the CPU oracle
+bit-exactly -- the whole filter bit array after bulk add, and every packed
+result bit of bulk contains -- on the same seeded keys (synth/), for every
+compiled schedule (variant x B x S x k x z x Θ x Φ x KPT x hash variant), the
+generic runtime-parameter kernel, and the edge cases (empty, ragged, unaligned
+inputs, non-power-of-two block counts, repeated adds, clear, seeds)."""
+import importlib.util
+import os
+from collections import defaultdict
+
+import numpy as np
+import pytest
+
+import synth
+from oracle.bfo import OracleFilter, unpack_bits
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _instances():
+    spec = importlib.util.spec_from_file_location(
+        "gen_instances", os.path.join(ROOT, "paper_2512_15595_b200", "csrc", "gen_instances.py"))
+    g = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(g)
+    return g.instances()
+
+
+def _groups():
+    grp = defaultdict(list)
+    for op, v, B, S, k, z, theta, phi, kpt, hv in _instances():
+        grp[(v, B, S, k, z)].append((op, theta, phi, kpt, hv))
+    return sorted(grp.items())
+
+
+GROUPS = _groups()
+
+
+def _to_dev(torch, a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(dev)
+
+
+def _gpu_bytes(f):
+    return f.data().cpu().numpy()
+
+
+def _gpu_contains(torch, f, qd):
+    out = f.contains(qd)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint32)
+
+
+# keys spanning several tiles with a ragged tail; small filter -> real collisions
+N_ADD, N_NEG = 6 * 1024 + 37, 4 * 1024 + 5
+
+
+@pytest.mark.parametrize("cfg,scheds", GROUPS, ids=[f"v{c[0]}_B{c[1]}_S{c[2]}_k{c[3]}_z{c[4]}" for c, _ in GROUPS])
+def test_every_compiled_schedule_matches_oracle(bflib, cuda, cfg, scheds):
+    import torch
+    bf = bflib
+    v, B, S, k, z = cfg
+    m = B * 997  # b = 997 blocks: not a power of two, heavy fill
+    keys = synth.keys(1000, N_ADD)
+    query = np.concatenate([keys[::3], synth.negatives(N_NEG)])
+    o = OracleFilter(v, m, B=B, S=S, k=k, z=z)
+    o.add(keys)
+    want_bytes = o.bytes()
+    want_res = o.contains(query)
+    kd, qd = _to_dev(torch, keys, cuda), _to_dev(torch, query, cuda)
+    f = bf.Filter(m, k, B, S, variant=v, z=z)
+    for op, theta, phi, kpt, hv in scheds:
+        f.set_layout(op, theta, phi, kpt, hv)
+        lay = f.layout(op)
+        assert lay["specialized"] == 1 and (lay["theta"], lay["phi"], lay["kpt"]) == (theta, phi, kpt)
+        if op == 0:
+            f.clear()
+            f.add(kd)
+            torch.cuda.synchronize()
+            got = _gpu_bytes(f)
+            assert np.array_equal(got, want_bytes), f"add schedule Θ={theta} Φ={phi} kpt={kpt} hv={hv}"
+    # contains schedules on the oracle-equal filter
+    f.set_layout(0, 0, 0)
+    f.clear()
+    f.add(kd)
+    for op, theta, phi, kpt, hv in scheds:
+        if op == 1:
+            f.set_layout(1, theta, phi, kpt, hv)
+            got = _gpu_contains(torch, f, qd)
+            assert np.array_equal(got, want_res), f"contains schedule Θ={theta} Φ={phi} kpt={kpt} hv={hv}"
+
+
+GENERIC = [  # no specialized instantiation -> generic runtime kernel
+    (3, 512, 64, 16, 0), (3, 1024, 64, 16, 0), (4, 1024, 64, 16, 4), (1, 512, 32, 20, 0),
+    (3, 256, 64, 20, 0), (2, 64, 64, 25, 0), (4, 512, 32, 12, 8), (1, 32, 32, 3, 0),
+    (3, 128, 32, 32, 0), (4, 256, 64, 8, 1),
+]
+
+
+@pytest.mark.parametrize("cfg", GENERIC, ids=[f"v{c[0]}_B{c[1]}_S{c[2]}_k{c[3]}_z{c[4]}" for c in GENERIC])
+def test_generic_kernel_matches_oracle(bflib, cuda, cfg):
+    import torch
+    bf = bflib
+    v, B, S, k, z = cfg
+    m = B * 1531
+    keys = synth.keys(7, N_ADD)
+    query = np.concatenate([keys[::2], synth.negatives(N_NEG)])
+    o = OracleFilter(v, m, B=B, S=S, k=k, z=z)
+    o.add(keys)
+    f = bf.Filter(m, k, B, S, variant=v, z=z)
+    assert f.layout(0)["specialized"] == 0 and f.layout(1)["specialized"] == 0
+    f.add(_to_dev(torch, keys, cuda))
+    torch.cuda.synchronize()
+    assert np.array_equal(_gpu_bytes(f), o.bytes())
+    assert np.array_equal(_gpu_contains(torch, f, _to_dev(torch, query, cuda)), o.contains(query))
+
+
+EDGE_CFGS = [(3, 256, 64, 8, 0), (1, 256, 64, 8, 0), (4, 256, 32, 8, 2), (2, 64, 64, 6, 0)]
+
+
+@pytest.mark.parametrize("cfg", EDGE_CFGS)
+@pytest.mark.parametrize("n", [0, 1, 31, 32, 33, 127, 128, 129, 1000, 4096 + 3])
+def test_sizes_and_tails(bflib, cuda, cfg, n):
+    import torch
+    bf = bflib
+    v, B, S, k, z = cfg
+    m = (1 << 16) + 3 * B
+    keys = synth.keys(50, n)
+    query = np.concatenate([keys, synth.negatives(n + 7)])
+    o = OracleFilter(v, m, B=B, S=S, k=k, z=z)
+    o.add(keys)
+    f = bf.Filter(m, k, B, S, variant=v, z=z)
+    f.add(_to_dev(torch, keys, cuda))
+    torch.cuda.synchronize()
+    assert np.array_equal(_gpu_bytes(f), o.bytes())
+    qd = _to_dev(torch, query, cuda)
+    out = torch.full(((query.size + 31) // 32 + 2,), -1, dtype=torch.int32, device=cuda)
+    bf.bf_contains(f.handle, qd, out, query.size)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.uint32)
+    nw = (query.size + 31) // 32
+    assert np.array_equal(got[:nw], o.contains(query))
+    assert (got[nw:] == 0xFFFFFFFF).all(), "wrote past ceil(n/32) words"
+    if query.size % 32:
+        assert got[nw - 1] >> (query.size % 32) == 0, "tail bits must be zero"
+
+
+@pytest.mark.parametrize("cfg", EDGE_CFGS)
+def test_unaligned_keys_idempotence_clear_seed(bflib, cuda, cfg):
+    import torch
+    bf = bflib
+    v, B, S, k, z = cfg
+    m = 1 << 18
+    keys = synth.keys(3, 10001)
+    buf = _to_dev(torch, np.concatenate([np.zeros(1, np.uint64), keys]), cuda)
+    kd = buf[1:]  # 8-byte aligned, not 16/32-byte aligned
+    assert kd.data_ptr() % 32 != 0
+    for seed in (0, 1, 0xDEADBEEF):
+        o = OracleFilter(v, m, B=B, S=S, k=k, z=z, seed=seed)
+        o.add(keys)
+        f = bf.Filter(m, k, B, S, variant=v, z=z, seed=seed)
+        for kpt in (1, 2, 4):
+            for op in (0, 1):
+                try:
+                    f.set_layout(op, *((B // S, 1) if op == 0 else (1, B // S)), kpt, 0)
+                except bf.BFError:
+                    continue
+            f.clear()
+            f.add(kd)
+            f.add(kd)  # idempotent
+            torch.cuda.synchronize()
+            assert np.array_equal(_gpu_bytes(f), o.bytes())
+            q = np.concatenate([keys[:999], synth.negatives(1001)])
+            qbuf = _to_dev(torch, np.concatenate([np.zeros(1, np.uint64), q]), cuda)
+            assert np.array_equal(_gpu_contains(torch, f, qbuf[1:]), o.contains(q))
+        f.clear()
+        torch.cuda.synchronize()
+        assert not _gpu_bytes(f).any()
+
+
+def test_streams_and_concurrent_adds(bflib, cuda):
+    """Two adds of disjoint halves on two streams == one add of all (OR commutes)."""
+    import torch
+    bf = bflib
+    keys = synth.keys(11, 200_003)
+    o = OracleFilter(3, 1 << 22, B=256, S=64, k=8)
+    o.add(keys)
+    f = bf.Filter(1 << 22, 8, 256, 64, "SBF")
+    kd = _to_dev(torch, keys, cuda)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        f.add(kd[:100_000])
+    with torch.cuda.stream(s2):
+        f.add(kd[100_000:])
+    torch.cuda.synchronize()
+    assert np.array_equal(_gpu_bytes(f), o.bytes())
+
+
+def test_host_buffer_path(bflib, cuda):
+    """bf_add_host / bf_contains_host (chunked, double-buffered) == oracle,
+    across a chunk boundary (chunks are 2^23 keys)."""
+    import torch
+    bf = bflib
+    n = (1 << 23) + 12345
+    keys = synth.keys(0, n)
+    o = OracleFilter(3, 1 << 26, B=256, S=64, k=8)
+    o.add(keys, threads=8)
+    hk = torch.from_numpy(keys.view(np.int64)).pin_memory()
+    f = bf.Filter(1 << 26, 8, 256, 64, "SBF")
+    f.add_host(hk)
+    assert np.array_equal(_gpu_bytes(f), o.bytes())
+    q = np.concatenate([keys[:1 << 22], synth.negatives((1 << 23) + 999)])
+    hq = torch.from_numpy(q.view(np.int64)).pin_memory()
+    out = f.contains_host(hq)
+    assert np.array_equal(out.numpy().view(np.uint32), o.contains(q, threads=8))
+
+
+def test_keygen_matches_synth(bflib, cuda):
+    import torch
+    bf = bflib
+    for base, n in [(0, 1), (0, 1000), (5, 1001), (synth.NEG_BASE, 4099)]:
+        out = torch.empty(n, dtype=torch.int64, device=cuda)
+        bf.bf_keygen(out, n, base)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), synth.keys(base, n))
+    # unaligned output
+    buf = torch.empty(1001, dtype=torch.int64, device=cuda)
+    bf.bf_keygen(buf[1:], 1000, 42)
+    torch.cuda.synchronize()
+    assert np.array_equal(buf[1:].cpu().numpy().view(np.uint64), synth.keys(42, 1000))
+
+
+@pytest.mark.parametrize("nsrc,nbytes", [(1, 8), (2, 4096), (3, 1 << 20), (8, (1 << 20) + 8)])
+def test_or_fold(bflib, cuda, nsrc, nbytes):
+    import torch
+    bf = bflib
+    rng = np.random.default_rng(nsrc)
+    stride = nbytes + 64 if nbytes % 16 else nbytes
+    src = rng.integers(0, 256, nsrc * stride, dtype=np.uint8)
+    want = np.zeros(nbytes, np.uint8)
+    for r in range(nsrc):
+        want |= src[r * stride: r * stride + nbytes]
+    sd = torch.from_numpy(src).to(cuda)
+    dst = torch.zeros(nbytes, dtype=torch.uint8, device=cuda)
+    bf.bf_or_fold(dst, sd, nsrc, stride, nbytes)
+    torch.cuda.synchronize()
+    assert np.array_equal(dst.cpu().numpy(), want)
+    # in place into source 0
+    bf.bf_or_fold(sd, sd, nsrc, stride, nbytes)
+    torch.cuda.synchronize()
+    assert np.array_equal(sd[:nbytes].cpu().numpy(), want)
+
+
+def test_probes_run(bflib, cuda):
+    import torch
+    bf = bflib
+    keys = torch.empty(1 << 16, dtype=torch.int64, device=cuda)
+    bf.bf_keygen(keys, keys.numel(), 0)
+    buf = torch.zeros(1 << 20, dtype=torch.uint8, device=cuda)
+    out = torch.empty(keys.numel() // 32, dtype=torch.int32, device=cuda)
+    bf.bf_probe_read(buf, (1 << 20) // 32, 256, keys, out)
+    bf.bf_probe_red(buf, (1 << 20) // 32, 256, 4, keys)
+    torch.cuda.synchronize()
+    assert buf.any()
+    n0 = bf.bf_launch_count()
+    bf.bf_probe_read(buf, (1 << 20) // 32, 256, keys, out)
+    assert bf.bf_launch_count() == n0 + 1
+
+
+def test_configs0_full_size(bflib, cuda):
+    """BASELINE configs[0] exactly: 2^20 keys into a 16 Mbit filter, B=256,
+    S=64, k=8, BBF and SBF; contains on 2^20 positives + 2^20 negatives."""
+    import torch
+    bf = bflib
+    n = 1 << 20
+    pos, neg = synth.positives(n), synth.negatives(n)
+    q = np.concatenate([pos, neg])
+    for v in (1, 3):
+        o = OracleFilter(v, 1 << 24, B=256, S=64, k=8)
+        o.add(pos, threads=8)
+        f = bf.Filter(1 << 24, 8, 256, 64, variant=v)
+        f.add(_to_dev(torch, pos, cuda))
+        torch.cuda.synchronize()
+        assert np.array_equal(_gpu_bytes(f), o.bytes())
+        got = _gpu_contains(torch, f, _to_dev(torch, q, cuda))
+        assert np.array_equal(got, o.contains(q, threads=8))
+        assert unpack_bits(got, 2 * n)[:n].all()
+
+
+def test_configs1_bench_workload_full_size(bflib, cuda):
+    """The bench workload (configs[1]: 32 MiB SBF 256/64 k=8, 2^26 keys) in the
+    launch configuration bench.py times: full bit array + all 2^26 results."""
+    import torch
+    bf = bflib
+    n = 1 << 26
+    kd = torch.empty(n, dtype=torch.int64, device=cuda)
+    bf.bf_keygen(kd, n, 0)
+    f = bf.Filter(1 << 28, 8, 256, 64, "SBF")
+    f.add(kd)
+    out = f.contains(kd)
+    torch.cuda.synchronize()
+    keys = synth.keys(0, n)
+    o = OracleFilter(3, 1 << 28, B=256, S=64, k=8)
+    o.add(keys, threads=os.cpu_count())
+    assert np.array_equal(_gpu_bytes(f), o.bytes())
+    assert (out.cpu().numpy().view(np.uint32) == 0xFFFFFFFF).all()  # all positives
+    negs = synth.negatives(1 << 22)
+    got = _gpu_contains(torch, f, _to_dev(torch, negs, cuda))
+    assert np.array_equal(got, o.contains(negs, threads=os.cpu_count()))
+
+
+def test_large_filter_offsets_sampled(bflib, cuda):
+    """An 8 GiB filter (configs[2]'s size; word offsets beyond 2^32 bytes):
+    oracle-built block ranges at the start, middle and end match exactly."""
+    import torch
+    bf = bflib
+    m = 1 << 36
+    n = 1 << 24
+    free, _ = torch.cuda.mem_get_info()
+    if free < (m // 8) + (1 << 30):
+        pytest.skip("not enough device memory")
+    kd = torch.empty(n, dtype=torch.int64, device=cuda)
+    bf.bf_keygen(kd, n, 0)
+    f = bf.Filter(m, 8, 256, 64, "SBF")
+    f.add(kd)
+    torch.cuda.synchronize()
+    keys = synth.keys(0, n)
+    o = OracleFilter(3, m, B=256, S=64, k=8, allocate=False)
+    b = o.b
+    data = f.data()
+    for lo in (0, b // 2 - 1000, b - 4096):
+        hi = lo + 4096
+        want = o.add_range(keys, lo, hi, threads=os.cpu_count())
+        got = data[lo * 32: hi * 32].cpu().numpy()
+        assert np.array_equal(got, want), lo
+    q = keys[:1 << 20]
+    out = f.contains(_to_dev(torch, q, cuda))
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy().view(np.uint32) == 0xFFFFFFFF).all()
