@@ -164,6 +164,17 @@ int bf_probe_read(const void* buf, uint64_t b, uint32_t block_bits, const uint64
 int bf_probe_red(void* buf, uint64_t b, uint32_t block_bits, uint32_t lanes,
                  const uint64_t* keys, uint64_t n, void* stream);
 
+/* Pure random-access probes: the same block geometry, but addresses come from
+ * an in-register xorshift stream (no key loads, no hashing), so they measure
+ * the memory system's random 32-byte-sector rate alone (the paper's GUPS
+ * speed of light).  red = 0: n block loads (widest loads,
+ * 4 in flight per thread); red = 1: n keys, each `lanes` lanes issuing one
+ * 64-bit red.global.or into their words of one random block.  The buffer's
+ * content is read or OR-ed; results are discarded.  n is rounded up to whole
+ * iterations of the grid. */
+int bf_probe_rng(void* buf, uint64_t b, uint32_t block_bits, int red, uint32_t lanes, uint64_t n,
+                 void* stream);
+
 /* Number of kernels this library has launched since load (all entry points).
  * Lets callers prove the CUDA path ran. */
 uint64_t bf_launch_count(void);

@@ -52,6 +52,7 @@ _SIGS = {
     "bf_keygen": (_i32, [_vp, _u64, _u64, _vp]),
     "bf_probe_read": (_i32, [_vp, _u64, _u32, _vp, _u64, _vp, _vp]),
     "bf_probe_red": (_i32, [_vp, _u64, _u32, _u32, _vp, _u64, _vp]),
+    "bf_probe_rng": (_i32, [_vp, _u64, _u32, _i32, _u32, _u64, _vp]),
     "bf_launch_count": (_u64, []),
     "bf_last_error": (C.c_char_p, [C.POINTER(_i32)]),
     "bf_version": (C.c_char_p, []),
@@ -174,6 +175,10 @@ def bf_probe_read(buf, b: int, block_bits: int, keys, out_bits, n: int | None = 
 def bf_probe_red(buf, b: int, block_bits: int, lanes: int, keys, n: int | None = None, stream=None) -> None:
     n = keys.numel() if n is None else n
     _check(_lib.bf_probe_red(_ptr(buf), b, block_bits, lanes, _ptr(keys), n, _stream(stream)))
+
+
+def bf_probe_rng(buf, b: int, block_bits: int, red: int, lanes: int, n: int, stream=None) -> None:
+    _check(_lib.bf_probe_rng(_ptr(buf), b, block_bits, red, lanes, n, _stream(stream)))
 
 
 def bf_launch_count() -> int:

@@ -508,4 +508,16 @@ int bf_probe_red(void* buf, uint64_t b, uint32_t block_bits, uint32_t lanes, con
     return check_launch("probe_red launch");
 }
 
+int bf_probe_rng(void* buf, uint64_t b, uint32_t block_bits, int red, uint32_t lanes, uint64_t n, void* stream)
+{
+    if (n == 0) return BF_OK;
+    if (!buf || b < 1 || b > (1ULL << 32) || block_bits < 64 || block_bits > 1024 || !is_pow2(block_bits) ||
+        (red && (!is_pow2(lanes) || lanes > block_bits / 64)))
+        return fail(BF_EINVAL, "bf_probe_rng: bad arguments");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    launch_probe_rng(buf, b, block_bits, red, red ? lanes : 1, n, (cudaStream_t)stream, 8 * sm_count(dev));
+    return check_launch("probe_rng launch");
+}
+
 }  // extern "C"

@@ -36,6 +36,9 @@ int launch_probe_read(const void* buf, uint64_t b, uint32_t B, const uint64_t* k
 void launch_probe_red(void* buf, uint64_t b, uint32_t B, uint32_t lanes, const uint64_t* keys, uint64_t n,
                       cudaStream_t st, int grid);
 
+void launch_probe_rng(const void* buf, uint64_t b, uint32_t B, int red, uint32_t lanes, uint64_t n,
+                      cudaStream_t st, int grid);
+
 struct Registrar {
     Registrar(void (*fn)()) { fn(); }
 };

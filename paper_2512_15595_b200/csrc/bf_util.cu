@@ -206,6 +206,80 @@ __global__ void __launch_bounds__(256) probe_red_kernel(unsigned long long* buf,
     }
 }
 
+// Pure random-access probes: addresses from an in-register xorshift stream,
+// no key loads, no hashing -- the memory system's random 32-byte-sector read
+// (LDG of the block) and sector-coalesced RED.OR rates (the GUPS-style
+// speed of light of P:L340, for this buffer's size and geometry).
+__device__ __forceinline__ uint64_t xs64(uint64_t x)
+{
+    x ^= x << 13;
+    x ^= x >> 7;
+    x ^= x << 17;
+    return x;
+}
+
+template <int NW>
+__global__ void __launch_bounds__(256) probe_read_rng_kernel(const unsigned long long* buf, uint64_t b,
+                                                             uint64_t iters, unsigned long long* sink)
+{
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t x = mix64(tid + 0x1234567ULL) | 1ULL;
+    unsigned long long acc = 0;
+    for (uint64_t it = 0; it < iters; ++it) {
+        unsigned long long w[4][NW < 4 ? 4 : NW];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            x = xs64(x);
+            const uint64_t blk = ((x >> 32) * b) >> 32;
+            if constexpr (NW == 1) VecLoad<64, 1>::run(buf + blk, w[j]);
+            else if constexpr (NW == 2) VecLoad<64, 2>::run(buf + blk * 2, w[j]);
+            else VecLoad<64, NW>::run(buf + blk * NW, w[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int i = 0; i < NW; ++i) acc += w[j][i];
+    }
+    if (acc == 0x9E3779B97F4A7C15ULL) sink[0] = acc;  // keeps the loads alive
+}
+
+__global__ void __launch_bounds__(256) probe_red_rng_kernel(unsigned long long* buf, uint64_t b, uint32_t nwords,
+                                                            uint32_t lanes, uint64_t iters)
+{
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t pos = lane & (lanes - 1);
+    const uint64_t group = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32 + (lane & ~(lanes - 1));
+    uint64_t x = mix64(group + 0x7654321ULL) | 1ULL;  // identical stream for the whole group
+    for (uint64_t it = 0; it < iters; ++it) {
+        x = xs64(x);
+        const uint64_t blk = ((x >> 32) * b) >> 32;
+        for (uint32_t w = pos; w < nwords; w += lanes)
+            red_or(buf + blk * nwords + w, 1ULL << ((x >> (6 * (w & 7))) & 63));
+    }
+}
+
+void launch_probe_rng(const void* buf, uint64_t b, uint32_t B, int red, uint32_t lanes, uint64_t n,
+                      cudaStream_t st, int grid)
+{
+    const uint64_t threads = (uint64_t)grid * 256;
+    if (red) {
+        const uint64_t groups = threads / lanes;
+        const uint64_t iters = (n + groups - 1) / groups;
+        probe_red_rng_kernel<<<grid, 256, 0, st>>>((unsigned long long*)buf, b, B / 64, lanes, iters);
+        return;
+    }
+    const uint64_t iters = (n + threads * 4 - 1) / (threads * 4);
+    unsigned long long* sink = (unsigned long long*)buf;
+    const unsigned long long* p = (const unsigned long long*)buf;
+    switch (B) {
+    case 64: probe_read_rng_kernel<1><<<grid, 256, 0, st>>>(p, b, iters, sink); break;
+    case 128: probe_read_rng_kernel<2><<<grid, 256, 0, st>>>(p, b, iters, sink); break;
+    case 512: probe_read_rng_kernel<8><<<grid, 256, 0, st>>>(p, b, iters, sink); break;
+    case 1024: probe_read_rng_kernel<16><<<grid, 256, 0, st>>>(p, b, iters, sink); break;
+    default: probe_read_rng_kernel<4><<<grid, 256, 0, st>>>(p, b, iters, sink); break;
+    }
+}
+
 int launch_probe_read(const void* buf, uint64_t b, uint32_t B, const uint64_t* keys, uint64_t n, uint32_t* out,
                       cudaStream_t st, int grid)
 {

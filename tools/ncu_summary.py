@@ -1,0 +1,83 @@
+#!/usr/bin/env python
+"""Summarise ncu output into profiles/ (tracked).
+
+    python tools/ncu_summary.py launches gpurun_out/launches_r1.csv  > profiles/r1_launches.md
+    python tools/ncu_summary.py full gpurun_out/prof_r1.ncu-rep        > profiles/r1_ncu_full.md
+"""
+from __future__ import annotations
+
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1TEX throughput %"),
+    ("l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed", "L1->XBAR request cycles %"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "L1 LSU data wavefronts %"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
+    ("lts__t_tag_requests.avg.pct_of_peak_sustained_elapsed", "L2 tag requests %"),
+    ("lts__t_requests_srcunit_tex_op_read.sum", "L2 read requests"),
+    ("lts__t_requests_srcunit_tex_op_red.sum", "L2 RED requests"),
+    ("lts__t_sectors_srcunit_tex_op_red.sum", "L2 RED sectors"),
+    ("lts__t_sector_hit_rate.pct", "L2 sector hit rate %"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
+    ("sm__cycles_elapsed.avg.per_second", "SM clock"),
+]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hi]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    d = defaultdict(list)
+    for r in rows[hi + 1:]:
+        d[r[ki]].append(float(r[vi].replace(",", "")) * (1e-3 if r[ui] == "ns" else 1.0))
+    tot = sum(sum(v) for v in d.values())
+    print(f"# ncu launch list: {path}\n")
+    print("Per-launch gpu__time_duration (cold-cache, serialised by ncu; compare shares, not absolutes).\n")
+    print("| kernel | launches | mean us | total us | share |")
+    print("|---|---|---|---|---|")
+    for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
+        print(f"| `{k[:110]}` | {len(v)} | {sum(v) / len(v):.1f} | {sum(v):.1f} | {100 * sum(v) / tot:.1f}% |")
+
+
+def full(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+    print(f"# ncu --set full summary: {path}\n")
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")]
+        print(f"## `{name}`\n")
+        print("| metric | value |")
+        print("|---|---|")
+        for key, label in KEYS:
+            if key in h:
+                i = h.index(key)
+                print(f"| {label} (`{key}`) | {r[i]} {units[i]} |")
+        items = []
+        for i, c in enumerate(h):
+            if c.startswith("smsp__pcsamp_warps_issue_stalled_") and not c.endswith("_not_issued"):
+                try:
+                    items.append((float(r[i].replace(",", "")), c))
+                except ValueError:
+                    pass
+        tot = sum(v for v, _ in items) or 1.0
+        print("\nTop stall reasons (PC sampling):\n")
+        for v, c in sorted(items, reverse=True)[:6]:
+            print(f"- {c.replace('smsp__pcsamp_warps_issue_stalled_', '')}: {100 * v / tot:.1f}%")
+        print()
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])

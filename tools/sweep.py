@@ -1,0 +1,133 @@
+#!/usr/bin/env python
+"""Schedule / configuration sweeps (BASELINE.json configs[1] and configs[3]).
+
+For every filter configuration selected and every compiled schedule (Θ, Φ,
+KPT, hash variant), time bulk add (into a cleared filter) and bulk contains
+(of the inserted keys) with CUDA events, median of --reps launches, and print
+one JSON line per (config, op, schedule).  Results are identical for every
+schedule (tests/test_gpu_parity.py); this only measures speed.
+
+    python tools/sweep.py --set c2      # configs[1]: 32 MiB, every block/k row, default layouts x KPT
+    python tools/sweep.py --set c4      # configs[3] grid: SBF 256/32 k=8,16, all Θ/Φ/KPT/hash variants
+    python tools/sweep.py --set c4l2    # the same grid on a 32 MiB (L2) filter
+"""
+from __future__ import annotations
+
+import argparse
+import importlib.util
+import json
+import os
+import statistics
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def instances():
+    spec = importlib.util.spec_from_file_location(
+        "gen_instances", os.path.join(ROOT, "paper_2512_15595_b200", "csrc", "gen_instances.py"))
+    g = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(g)
+    return g.instances()
+
+
+def c_iso(variant, B, S, k, z, fpr=1e-4):
+    """bits/key at the target FPR from the exact model (oracle/fpr_model)."""
+    from oracle import fpr_model as M
+    lo, hi = 4.0, 200.0
+    b = 1 << 20
+    for _ in range(50):
+        c = (lo + hi) / 2
+        n = int(b * B / c)
+        if M.fpr_exact(variant, n, b, B, S, k, z) > fpr:
+            lo = c
+        else:
+            hi = c
+    return hi
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--set", default="c2", choices=["c2", "c4", "c4l2", "one"])
+    ap.add_argument("--n", type=int, default=1 << 26)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--cfg", default=None, help="v,B,S,k,z for --set one")
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+
+    import torch
+
+    from paper_2512_15595_b200 import bf
+
+    dev = torch.device("cuda:0")
+    inst = instances()
+    groups = defaultdict(list)
+    for op, v, B, S, k, z, th, ph, kpt, hv in inst:
+        groups[(v, B, S, k, z)].append((op, th, ph, kpt, hv))
+    if a.set == "c2":
+        sel = {c: s for c, s in groups.items() if 4 <= c[3] <= 16 and c[1] <= 256}
+        m_of = lambda c: 1 << 28  # noqa: E731
+        n = a.n
+    elif a.set in ("c4", "c4l2"):
+        sel = {c: s for c, s in groups.items() if c[:3] == (3, 256, 32) and c[3] in (8, 16)}
+        if a.set == "c4":
+            # m = c_iso(1e-4) * 2^30 bits (~3.3 GiB, b not a power of two)
+            m_of = lambda c: int(c_iso(c[0], c[1], c[2], c[3], c[4]) * (1 << 30))  # noqa: E731
+            n = 1 << 30
+        else:
+            m_of = lambda c: 1 << 28  # noqa: E731
+            n = 1 << 30
+    else:
+        c = tuple(int(x) for x in a.cfg.split(","))
+        sel = {c: groups[c]}
+        m_of = lambda c: 1 << 28  # noqa: E731
+        n = a.n
+
+    keys = torch.empty(n, dtype=torch.int64, device=dev)
+    bf.bf_keygen(keys, n, 0)
+    out = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fh = open(a.out, "a") if a.out else None
+    for cfg, scheds in sorted(sel.items()):
+        v, B, S, k, z = cfg
+        m = m_of(cfg)
+        f = bf.Filter(m, k, B, S, v, z=z)
+        for op, th, ph, kpt, hv in sorted(scheds):
+            f.set_layout(op, th, ph, kpt, hv)
+            ts = []
+            for r in range(a.reps + 1):
+                if op == 0:
+                    f.clear()
+                e0.record(st)
+                if op == 0:
+                    f.add(keys)
+                else:
+                    f.contains(keys, out)
+                e1.record(st)
+                torch.cuda.synchronize()
+                if r:
+                    ts.append(e0.elapsed_time(e1))
+            t = statistics.median(ts)
+            rec = {"set": a.set, "variant": v, "B": B, "S": S, "k": k, "z": z, "m_bits": m, "n": n,
+                   "op": "add" if op == 0 else "contains", "theta": th, "phi": ph, "kpt": kpt, "hv": hv,
+                   "ms": round(t, 4), "gkeys_s": round(n / (t * 1e-3) / 1e9, 3)}
+            print(json.dumps(rec), flush=True)
+            if fh:
+                fh.write(json.dumps(rec) + "\n")
+        # restore default and check all-true after the sweep (sanity)
+        f.set_layout(0, 0, 0)
+        f.set_layout(1, 0, 0)
+        f.clear()
+        f.add(keys)
+        f.contains(keys, out)
+        torch.cuda.synchronize()
+        if n % 32 == 0:
+            assert int((out != -1).sum()) == 0, f"false negatives in {cfg}"
+        del f
+
+
+if __name__ == "__main__":
+    main()
