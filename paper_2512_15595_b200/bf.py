@@ -15,7 +15,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbf200.so")
+LIB_PATH = os.environ.get("BF200_LIB") or os.path.join(_HERE, "libbf200.so")  # override: A/B experiments
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "bf.h")
 
 if not os.path.exists(LIB_PATH):

@@ -167,7 +167,7 @@ static int set_sched(bf_filter* f, int op, int theta, int phi, int kpt, int hv)
     if (theta == 0) {  // defaults
         if (op == 0) { theta = s; phi = 1; }
         else { theta = 1; phi = s; }
-        kpt = (op == 0) ? 1 : 4;
+        kpt = 4;  // 4 keys per lane: one 256-bit key load, 4 blocks in flight (profiles/r1_sweep_c2.md)
         hv = 0;
     }
     if (!is_pow2(theta) || !is_pow2(phi) || theta * phi > s || theta > 32)
@@ -332,6 +332,7 @@ static Params make_params(const bf_filter* f, const uint64_t* keys, uint64_t n, 
     Params p;
     p.words = f->words;
     p.b = f->b;
+    p.b32 = (uint32_t)f->b;
     p.keys = keys;
     p.n = n;
     p.out = out;

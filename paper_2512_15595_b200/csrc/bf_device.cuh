@@ -97,10 +97,13 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x)
     return z ^ (z >> 31);
 }
 
-// Block index: Parquet fast range on the high half, b <= 2^32.
-__device__ __forceinline__ uint32_t block_of(uint64_t h, uint64_t b)
+// Block index: Parquet fast range on the high half, ((h >> 32) * b) >> 32
+// with b <= 2^32.  b travels as b32 = b mod 2^32 (0 means 2^32,
+// where the block is h >> 32 itself), so the product is one IMAD.HI.
+__device__ __forceinline__ uint32_t block_of(uint64_t h, uint32_t b32)
 {
-    return (uint32_t)(((h >> 32) * b) >> 32);
+    const uint32_t hi = (uint32_t)(h >> 32);
+    return b32 ? __umulhi(hi, b32) : hi;
 }
 
 // ---------------------------------------------------------------- words

@@ -38,6 +38,7 @@ namespace bf {
 struct Params {
     void* words;           // filter word array (b * s words of S bits)
     uint64_t b;            // number of blocks
+    uint32_t b32;          // b mod 2^32 (0 <=> b == 2^32), for the block index
     const uint64_t* keys;  // device keys
     uint64_t n;            // number of keys
     uint32_t* out;         // contains: ceil(n/32) result words
@@ -56,6 +57,10 @@ struct Cfg {
     static constexpr int Q = (V == V_SBF || V == V_RBBF) ? K / s : (V == V_CSBF ? K / Z : K);
     static constexpr int STEPS = s / (THETA * PHI);
     static constexpr int NSLOT = STEPS * PHI;  // words per lane
+    // Θ=1 contains loads the next tile's keys while this tile's blocks are in
+    // flight only when the KPT loaded blocks leave room for them
+    // (KPT*s*S/32 registers); add and cooperative contains always do
+    static constexpr bool PREFETCH_T1 = (KPT * s * S / 32 <= 16);
     using W = typename WordT<S>::T;
 
     static_assert(S == 32 || S == 64, "word size");
@@ -296,9 +301,31 @@ __device__ __forceinline__ void store_results(uint32_t* out, uint64_t tile, uint
 }
 
 // ----------------------------------------------------------------- tile
+// Keys of a full tile for this lane: one 128/256-bit load when the key array
+// is aligned for it, KPT 64-bit loads otherwise.
+template <int KPT>
+__device__ __forceinline__ void load_tile_keys(const uint64_t* keys, uint64_t mine, bool vec_ok,
+                                               uint64_t (&key)[KPT])
+{
+    if (vec_ok) {
+        if constexpr (KPT == 4) ld_keys4(keys + mine, key);
+        else if constexpr (KPT == 2) ld_keys2(keys + mine, key);
+        else key[0] = ld_key1(keys + mine);
+    } else {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) key[j] = ld_key1(keys + mine + j);
+    }
+}
+
+// One tile of 32*KPT keys.  Full tiles arrive with their keys already in
+// registers (kin); the keys of this warp's next full tile are loaded into
+// knext while this tile's memory accesses are in flight (software pipeline:
+// the HBM latency of the key stream hides behind a whole tile of work).
 template <class C, bool ADD, bool FULL>
 __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_t lane, uint32_t pos,
-                                         uint32_t gbase, bool vec_ok, const SaltSrc<C>& ss)
+                                         uint32_t gbase, bool vec_ok, const SaltSrc<C>& ss,
+                                         const uint64_t (&kin)[C::KPT], uint64_t (&knext)[C::KPT],
+                                         bool have_next, uint64_t next_mine)
 {
     using W = typename C::W;
     constexpr int KPT = C::KPT;
@@ -306,18 +333,19 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
     const uint64_t mine = base + (uint64_t)lane * KPT;
 
     // (1) ingest + hash once per key
+    constexpr bool PF = ADD || C::THETA > 1 || C::PREFETCH_T1;
     uint64_t key[KPT];
     bool valid[KPT];
-    if (FULL && vec_ok) {
-        if constexpr (KPT == 4) ld_keys4(p.keys + mine, key);
-        else if constexpr (KPT == 2) ld_keys2(p.keys + mine, key);
-        else key[0] = ld_key1(p.keys + mine);
+    if constexpr (!PF) {
+        if (FULL) load_tile_keys<KPT>(p.keys, mine, vec_ok, key);
+    }
 #pragma unroll
-        for (int j = 0; j < KPT; ++j) valid[j] = true;
-    } else {
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) {
-            valid[j] = FULL || (mine + j < p.n);
+    for (int j = 0; j < KPT; ++j) {
+        if (FULL) {
+            valid[j] = true;
+            if constexpr (PF) key[j] = kin[j];
+        } else {
+            valid[j] = mine + j < p.n;
             key[j] = valid[j] ? ld_key1(p.keys + mine + j) : 0ULL;
         }
     }
@@ -327,22 +355,29 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
         for (int j = 0; j < KPT; ++j) {
             const uint64_t h = xxh64_u64(key[j], p.seed);
             lo[j] = (uint32_t)h;
-            blk[j] = block_of(h, p.b);
+            blk[j] = block_of(h, p.b32);
         }
     }
 
     uint32_t res = 0;
+    if constexpr (ADD || C::THETA > 1) {
+        if (have_next) load_tile_keys<KPT>(p.keys, next_mine, vec_ok, knext);
+    }
     if constexpr (C::THETA == 1 && ADD) {
 #pragma unroll
         for (int j = 0; j < KPT; ++j)
             if (FULL || valid[j]) add_part<C>((W*)p.words, lo[j], blk[j], 0, ss);
     } else if constexpr (C::THETA == 1) {
         // issue every block load of the tile before testing any (memory-level
-        // parallelism: KPT*s/Φ loads in flight per lane)
+        // parallelism: KPT*s/Φ loads in flight per lane), then the next
+        // tile's keys, then test
         W wd[KPT][C::s];
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
             if (FULL || valid[j]) load_block<C>((const W*)p.words, blk[j], wd[j]);
+        }
+        if constexpr (C::PREFETCH_T1) {
+            if (have_next) load_tile_keys<KPT>(p.keys, next_mine, vec_ok, knext);
         }
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
@@ -363,7 +398,7 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
                     v = FULL || idx < p.n;
                     const uint64_t h = xxh64_u64(v ? p.keys[idx] : 0ULL, p.seed);
                     l = (uint32_t)h;
-                    bk = block_of(h, p.b);
+                    bk = block_of(h, p.b32);
                 } else {
                     l = __shfl_sync(0xffffffffu, lo[j], src);
                     bk = __shfl_sync(0xffffffffu, blk[j], src);
@@ -407,9 +442,23 @@ __global__ void __launch_bounds__(256) bulk_kernel(const Params p)
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const bool vec_ok = (((uintptr_t)p.keys) & (8 * C::KPT - 1)) == 0;
+    constexpr bool PF = ADD || C::THETA > 1 || C::PREFETCH_T1;
+    uint64_t kcur[C::KPT] = {};
+    if (PF && gw < nfull) load_tile_keys<C::KPT>(p.keys, gw * TILE + lane * C::KPT, vec_ok, kcur);
     for (uint64_t t = gw; t < ntiles; t += nw) {
-        if (t < nfull) run_tile<C, ADD, true>(p, t, lane, pos, gbase, vec_ok, ss);
-        else run_tile<C, ADD, false>(p, t, lane, pos, gbase, vec_ok, ss);
+        const uint64_t tn = t + nw;
+        const bool have_next = tn < nfull;
+        uint64_t knext[C::KPT];
+        if (t < nfull)
+            run_tile<C, ADD, true>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
+                                   tn * TILE + lane * C::KPT);
+        else
+            run_tile<C, ADD, false>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
+                                    tn * TILE + lane * C::KPT);
+        if constexpr (PF) {
+#pragma unroll
+            for (int j = 0; j < C::KPT; ++j) kcur[j] = knext[j];
+        }
     }
 }
 

@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) generic_kernel(const Params p)
         bool ok = false;
         if (valid) {
             const uint64_t h = xxh64_u64(p.keys[i], p.seed);
-            const uint32_t lo = (uint32_t)h, blk = block_of(h, p.b);
+            const uint32_t lo = (uint32_t)h, blk = block_of(h, p.b32);
             W* bp = (W*)p.words + (uint64_t)blk * s;
             ok = true;
             for (uint32_t w = 0; w < s; ++w) {
