@@ -56,14 +56,17 @@ def parse():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--z", type=int, default=None)
     ap.add_argument("--n", type=int, default=None, help="keys per rank (override)")
+    ap.add_argument("--m-bits", dest="m_bits", type=int, default=None, help="filter bits (override)")
+    ap.add_argument("--range-mib", type=int, default=0, help="binned add: filter MiB per range (0: library default)")
     ap.add_argument("--merge", choices=["alltoall", "allgather"], default="alltoall")
+    ap.add_argument("--add-mode", choices=["auto", "direct", "binned"], default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
     cfg = dict(CONFIGS[a.config])
-    for key in ("variant", "B", "S", "k", "z", "n"):
+    for key in ("variant", "B", "S", "k", "z", "n", "m_bits"):
         if getattr(a, key) is not None:
             cfg[key] = getattr(a, key)
     return a, cfg
@@ -194,6 +197,8 @@ def run_ours(a, cfg, rank, world, local_rank):
     torch.cuda.set_device(dev)
     n = cfg["n"]
     f = bf.Filter(cfg["m_bits"], cfg["k"], cfg["B"], cfg["S"], cfg["variant"], z=cfg["z"])
+    f.set_add_mode({"auto": bf.BF_ADD_AUTO, "direct": bf.BF_ADD_DIRECT, "binned": bf.BF_ADD_BINNED}[a.add_mode],
+                   a.range_mib << 20)
     keys = torch.empty(n, dtype=torch.int64, device=dev)
     bf.bf_keygen(keys, n, rank * n)  # rank r's shard of the positive set
     out = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
@@ -285,6 +290,7 @@ def run_ours(a, cfg, rank, world, local_rank):
                    "keys_per_step": 2 * n * world, "parallelism": f"dp{world} (replicated filter)",
                    "merge": a.merge if world > 1 else None,
                    "layout_add": f.layout(0), "layout_contains": f.layout(1),
+                   "add_path": "binned" if f.add_mode()[1] else "direct",
                    "l2": f"inputs larger than L2 ({n * 8 >> 20} MiB keys streamed per kernel); "
                          f"filter {cfg['residency']}-resident by design"},
         "add_gkeys_s": round(n / (t_add * 1e-3) / 1e9, 3),

@@ -131,6 +131,27 @@ int bf_geometry(const bf_filter* f, uint64_t* b, uint32_t* s, uint64_t* m_eff_bi
  * is not compiled for this (variant, B, S, k, z). */
 int bf_set_layout(bf_filter* f, int op, int theta, int phi, int kpt, int hash_variant);
 
+/* Bulk-add strategy for filters larger than L2 (HBM-resident).
+ *   BF_ADD_DIRECT  every key's pattern is OR-ed straight into the filter
+ *                  (one random HBM read-modify-write per key: the paper's
+ *                  GUPS-bound regime).
+ *   BF_ADD_BINNED  keys are hashed once and binned by filter range into a
+ *                  device scratch buffer (range_bytes of filter per bin),
+ *                  then each range is applied while it is L2-resident.  Same
+ *                  bits (OR commutes); HBM traffic per key drops to
+ *                  streaming.  Scratch: ~8 bytes per key of a batch of at most
+ *                  max_batch_keys keys, owned by the filter, freed in
+ *                  bf_destroy.
+ *   BF_ADD_AUTO    binned when the filter is >= 96 MiB and n*8 >= its size
+ *                  (default).
+ * range_bytes / max_batch_keys = 0 choose the defaults (32 MiB, 2^31).
+ * BF_EUNSUPPORTED if the binned kernels are not compiled for this
+ * configuration and its add schedule. */
+enum { BF_ADD_AUTO = 0, BF_ADD_DIRECT = 1, BF_ADD_BINNED = 2 };
+int bf_set_add_mode(bf_filter* f, int mode, uint64_t range_bytes, uint64_t max_batch_keys);
+/* mode set by bf_set_add_mode, and whether the most recent bf_add was binned. */
+int bf_get_add_mode(const bf_filter* f, int* mode, int* last_binned);
+
 /* Current schedule of `op` and whether it runs a specialized (compile-time
  * k/B/S) kernel (1) or the generic runtime-parameter kernel (0). */
 int bf_get_layout(const bf_filter* f, int op, int* theta, int* phi, int* kpt,

@@ -53,6 +53,8 @@ _SIGS = {
     "bf_probe_read": (_i32, [_vp, _u64, _u32, _vp, _u64, _vp, _vp]),
     "bf_probe_red": (_i32, [_vp, _u64, _u32, _u32, _vp, _u64, _vp]),
     "bf_probe_rng": (_i32, [_vp, _u64, _u32, _i32, _u32, _u64, _vp]),
+    "bf_set_add_mode": (_i32, [_vp, _i32, _u64, _u64]),
+    "bf_get_add_mode": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
     "bf_launch_count": (_u64, []),
     "bf_last_error": (C.c_char_p, [C.POINTER(_i32)]),
     "bf_version": (C.c_char_p, []),
@@ -158,6 +160,19 @@ def bf_get_layout(f: int, op: int) -> dict:
     return dict(zip(("theta", "phi", "kpt", "hash_variant", "specialized"), (int(x.value) for x in v)))
 
 
+BF_ADD_AUTO, BF_ADD_DIRECT, BF_ADD_BINNED = 0, 1, 2
+
+
+def bf_set_add_mode(f: int, mode: int, range_bytes: int = 0, max_batch_keys: int = 0) -> None:
+    _check(_lib.bf_set_add_mode(f, mode, range_bytes, max_batch_keys))
+
+
+def bf_get_add_mode(f: int) -> tuple[int, int]:
+    m, last = _i32(), _i32()
+    _check(_lib.bf_get_add_mode(f, C.byref(m), C.byref(last)))
+    return int(m.value), int(last.value)
+
+
 def bf_or_fold(dst, srcs, nsrc: int, src_stride_bytes: int, nbytes: int, stream=None) -> None:
     _check(_lib.bf_or_fold(_ptr(dst), _ptr(srcs), nsrc, src_stride_bytes, nbytes, _stream(stream)))
 
@@ -239,6 +254,13 @@ class Filter:
 
     def set_layout(self, op: int, theta: int, phi: int, kpt: int = 1, hash_variant: int = 0):
         bf_set_layout(self.handle, op, theta, phi, kpt, hash_variant)
+
+    def set_add_mode(self, mode: int, range_bytes: int = 0, max_batch_keys: int = 0):
+        bf_set_add_mode(self.handle, mode, range_bytes, max_batch_keys)
+
+    def add_mode(self) -> tuple[int, int]:
+        """(mode, whether the last add took the binned path)."""
+        return bf_get_add_mode(self.handle)
 
     def layout(self, op: int) -> dict:
         return bf_get_layout(self.handle, op)

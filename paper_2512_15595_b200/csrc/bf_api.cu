@@ -13,6 +13,7 @@
 
 #include "../../include/bf.h"
 #include "bf_internal.h"
+#include "bf_binned.cuh"
 #include "bf_kernels.cuh"
 
 #define BF_VERSION "bf200 1.0 (sm_100a)"
@@ -127,6 +128,15 @@ struct bf_filter {
     uint64_t stage_n;
     cudaStream_t copy_stream;
     cudaEvent_t ev_ready[2], ev_free[2];
+    // binned add (HBM-resident filters, csrc/bf_binned.cuh)
+    int add_mode;           // BF_ADD_AUTO / BF_ADD_DIRECT / BF_ADD_BINNED
+    int last_add_binned;    // path the last bf_add took
+    uint64_t range_bytes;   // filter bytes per bin range (0: default)
+    uint64_t max_batch;     // keys binned per batch (0: default)
+    uint64_t* recs;
+    uint64_t recs_bytes;
+    unsigned long long* cursor;
+    uint32_t cursor_n;
 };
 
 static int validate(uint64_t m_bits, uint32_t k, uint32_t B, uint32_t S, uint32_t variant, uint32_t* z_out)
@@ -277,6 +287,8 @@ void bf_destroy(bf_filter* f)
     if (!f) return;
     DeviceGuard g(f->device);
     free_staging(f);
+    if (f->recs) cudaFree(f->recs);
+    if (f->cursor) cudaFree(f->cursor);
     cudaFree(f->words);
     delete f;
 }
@@ -360,12 +372,140 @@ static int launch_bulk(const bf_filter* f, int op, const uint64_t* keys, uint64_
     return check_launch(op ? "contains launch" : "add launch");
 }
 
+// ------------------------------------------------------------ binned add
+static const uint64_t kDefaultRangeBytes = 32ULL << 20;  // one L2-resident range
+static const uint64_t kDefaultMaxBatch = 1ULL << 31;     // 16 GiB of records
+static const uint64_t kBinMinFilterBytes = 96ULL << 20;  // below this the filter lives in L2
+
+static bool binned_available(const bf_filter* f, KernelFn* bin, KernelFn* apply)
+{
+    const Sched& sc = f->sched[0];
+    if (!sc.specialized) return false;
+    InstKey kb{2, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z, 1, 1, 1, 0};
+    InstKey ka{3, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z,
+               (uint8_t)sc.theta, (uint8_t)sc.phi, (uint8_t)sc.kpt, (uint8_t)sc.hv};
+    *bin = registry_find(kb);
+    *apply = registry_find(ka);
+    return *bin && *apply;
+}
+
+static int binned_add(bf_filter* f, const uint64_t* keys, uint64_t n, cudaStream_t st, KernelFn bin_fn,
+                      KernelFn apply_fn)
+{
+    const uint64_t blk_bytes = f->B / 8;
+    uint64_t range_bytes = f->range_bytes ? f->range_bytes : kDefaultRangeBytes;
+    uint32_t lg = 0;
+    while ((blk_bytes << (lg + 1)) <= range_bytes) ++lg;  // blocks per range = 2^lg
+    uint64_t R = (f->b + (1ULL << lg) - 1) >> lg;
+    while (R > 4096) {  // keep the per-CTA histogram small
+        ++lg;
+        R = (f->b + (1ULL << lg) - 1) >> lg;
+    }
+    const uint64_t batch = n < (f->max_batch ? f->max_batch : kDefaultMaxBatch) ? n
+                                                                              : (f->max_batch ? f->max_batch : kDefaultMaxBatch);
+    uint64_t cap = batch / R + batch / R / 32 + 8192;  // mean + 3% + slack (sd ~ sqrt(mean))
+    cap = (cap + 127) & ~127ULL;
+    const uint64_t need = R * cap * 8;
+    cudaError_t e = cudaSuccess;
+    if (f->recs_bytes < need) {
+        if (f->recs) cudaFree(f->recs);
+        f->recs = nullptr;
+        f->recs_bytes = 0;
+        e = cudaMalloc(&f->recs, need);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(BF_ENOMEM, "binned add scratch (%llu bytes): %s", (unsigned long long)need, cudaGetErrorString(e));
+        }
+        f->recs_bytes = need;
+    }
+    if (f->cursor_n < R) {
+        if (f->cursor) cudaFree(f->cursor);
+        f->cursor = nullptr;
+        e = cudaMalloc(&f->cursor, R * sizeof(unsigned long long));
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(BF_ENOMEM, "binned add counters: %s", cudaGetErrorString(e));
+        }
+        f->cursor_n = (uint32_t)R;
+    }
+    const size_t smem = bin_smem_bytes((uint32_t)R);
+    cudaFuncSetAttribute((const void*)bin_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)bin_fn, BIN_THREADS, smem) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    const int grid_bin = per_sm * sm_count(f->device);
+    const int grid_apply = pick_grid(f, apply_fn);
+    for (uint64_t off = 0; off < n; off += batch) {
+        const uint64_t cnt = n - off < batch ? n - off : batch;
+        BinParams bp;
+        bp.f = make_params(f, keys + off, cnt, nullptr);
+        bp.recs = f->recs;
+        bp.cursor = f->cursor;
+        bp.cap = cap;
+        bp.lg_bpr = lg;
+        bp.nranges = (uint32_t)R;
+        bp.range = 0;
+        if ((e = cudaMemsetAsync(f->cursor, 0, R * sizeof(unsigned long long), st)) != cudaSuccess)
+            return cuda_fail(e, "binned add: cursor reset");
+        void* args[] = {&bp};
+        uint64_t chunks = (cnt + BIN_CHUNK - 1) / BIN_CHUNK;
+        const unsigned gb = (unsigned)(chunks < (uint64_t)grid_bin ? chunks : grid_bin);
+        if ((e = cudaLaunchKernel((const void*)bin_fn, dim3(gb), dim3(BIN_THREADS), args, smem, st)) != cudaSuccess)
+            return cuda_fail(e, "bin launch");
+        if (int rc = check_launch("bin launch")) return rc;
+        // one launch per range: the GPU stays inside one L2-resident range
+        const uint64_t tiles = (cap + 32 * f->sched[0].kpt - 1) / (32 * f->sched[0].kpt);
+        uint64_t ga = (tiles + 7) / 8;
+        if (ga > (uint64_t)grid_apply) ga = grid_apply;
+        for (uint32_t r = 0; r < (uint32_t)R; ++r) {
+            bp.range = r;
+            if ((e = cudaLaunchKernel((const void*)apply_fn, dim3((unsigned)ga), dim3(256), args, 0, st)) != cudaSuccess)
+                return cuda_fail(e, "apply launch");
+            if (int rc = check_launch("apply launch")) return rc;
+        }
+    }
+    return BF_OK;
+}
+
+int bf_set_add_mode(bf_filter* f, int mode, uint64_t range_bytes, uint64_t max_batch_keys)
+{
+    if (!f || mode < BF_ADD_AUTO || mode > BF_ADD_BINNED) return fail(BF_EINVAL, "bad filter or add mode");
+    if (range_bytes && range_bytes < (uint64_t)f->B / 8) return fail(BF_EINVAL, "range_bytes smaller than a block");
+    if (mode == BF_ADD_BINNED) {
+        KernelFn a, b;
+        if (!binned_available(f, &b, &a))
+            return fail(BF_EUNSUPPORTED, "binned add is not compiled for this configuration / add schedule");
+    }
+    f->add_mode = mode;
+    f->range_bytes = range_bytes;
+    f->max_batch = max_batch_keys;
+    return BF_OK;
+}
+
+int bf_get_add_mode(const bf_filter* f, int* mode, int* last_binned)
+{
+    if (!f) return fail(BF_EINVAL, "null filter");
+    if (mode) *mode = f->add_mode;
+    if (last_binned) *last_binned = f->last_add_binned;
+    return BF_OK;
+}
+
 int bf_add(bf_filter* f, const uint64_t* keys, uint64_t n, void* stream)
 {
     if (!f) return fail(BF_EINVAL, "null filter");
     if (n == 0) return BF_OK;
     if (!keys || ((uintptr_t)keys & 7)) return fail(BF_EINVAL, "keys must be a non-null 8-byte-aligned device pointer");
     DeviceGuard g(f->device);
+    KernelFn bin_fn = nullptr, apply_fn = nullptr;
+    const bool want_binned =
+        f->add_mode == BF_ADD_BINNED ||
+        (f->add_mode == BF_ADD_AUTO && f->bytes >= kBinMinFilterBytes && n * 8 >= f->bytes);
+    if (want_binned && binned_available(f, &bin_fn, &apply_fn)) {
+        f->last_add_binned = 1;
+        return binned_add(f, keys, n, (cudaStream_t)stream, bin_fn, apply_fn);
+    }
+    f->last_add_binned = 0;
     return launch_bulk(f, 0, keys, n, nullptr, (cudaStream_t)stream);
 }
 

@@ -1,0 +1,222 @@
+// bf_binned.cuh -- bulk add for filters much larger than L2 (HBM-resident).
+//
+// Direct bulk add on an HBM-resident filter pays one random DRAM
+// read-modify-write of a sector per key (the paper's GUPS-bound regime,
+// P:L340-346).  Because OR commutes the keys can be applied in any
+// order, so this path first BINS them by filter range and then applies each
+// range while it is L2-resident:
+//
+//   phase 1 (bin_kernel):   hash every key once; record = (block << 32) | lo;
+//                           scatter the records into per-range buckets
+//                           (CTA-local counting sort in shared memory, one
+//                           global atomic per range per CTA chunk, coalesced
+//                           runs).  HBM streaming: 8 B in + 8 B out per key.
+//   phase 2 (apply_kernel): walk the buckets range-major; a range (a few tens
+//                           of MiB) stays in L2 while every CTA ORs its
+//                           records into it with the same cooperative
+//                           red.global.or as the direct kernel (no hashing:
+//                           the record carries block and lo).  HBM: 8 B per
+//                           key + each filter line read once and written
+//                           back once.
+//
+// The filter bits are exactly those of the direct kernel (same block, same
+// pattern, OR is order-free); tests/test_gpu_parity.py checks them against
+// the oracle.  Records that do not fit a bucket (capacity n/R + slack; never
+// reached with uniform hashes) are ORed in directly by phase 1.
+#pragma once
+
+#include "bf_kernels.cuh"
+
+namespace bf {
+
+struct BinParams {
+    Params f;                    // filter (words, b, b32, seed) + keys/n to bin
+    uint64_t* recs;              // nranges * cap records
+    unsigned long long* cursor;  // nranges reservation counters (zeroed per batch)
+    uint64_t cap;                // records per bucket
+    uint32_t lg_bpr;             // log2(blocks per range)
+    uint32_t nranges;
+    uint32_t range;              // phase 2: the range this launch applies
+};
+
+constexpr int BIN_THREADS = 256;
+constexpr int BIN_KPT = 8;
+constexpr int BIN_CHUNK = BIN_THREADS * BIN_KPT;  // keys per CTA chunk
+
+// dynamic smem layout: stage[CHUNK] u64 | hist[R] u32 (+pad) | gbase[R] u64 | stage_r[CHUNK] u16
+__host__ __device__ inline size_t bin_smem_bytes(uint32_t nranges)
+{
+    return (size_t)BIN_CHUNK * 8 + (size_t)(nranges + 1) * 4 + (size_t)nranges * 8 + (size_t)BIN_CHUNK * 2;
+}
+
+// exclusive scan of a[0..n) in shared memory (n <= 256*32), returns the total
+template <int NT>
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t* a, uint32_t n, uint32_t* warp_tot)
+{
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t per = (n + NT - 1) / NT;
+    const uint32_t lo = tid * per, hi = min(n, lo + per);
+    uint32_t sum = 0;
+    for (uint32_t i = lo; i < hi; ++i) sum += a[i];
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += v;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t v = lane < NT / 32 ? warp_tot[lane] : 0;
+        uint32_t iv = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, iv, o);
+            if (lane >= (uint32_t)o) iv += u;
+        }
+        if (lane < NT / 32) warp_tot[lane] = iv - v;  // exclusive warp offsets
+        if (lane == NT / 32 - 1) warp_tot[NT / 32] = iv;
+    }
+    __syncthreads();
+    uint32_t run = warp_tot[warp] + incl - sum;
+    for (uint32_t i = lo; i < hi; ++i) {
+        const uint32_t v = a[i];
+        a[i] = run;
+        run += v;
+    }
+    const uint32_t total = warp_tot[NT / 32];
+    __syncthreads();
+    return total;
+}
+
+// Phase 1.  C1 is the Θ=1 configuration of the filter (for the overflow path).
+template <class C1>
+__global__ void __launch_bounds__(BIN_THREADS) bin_kernel(const BinParams bp)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t R = bp.nranges;
+    uint64_t* stage = (uint64_t*)smem;
+    uint32_t* hist = (uint32_t*)(stage + BIN_CHUNK);
+    unsigned long long* gbase = (unsigned long long*)(hist + R + (R & 1));
+    uint16_t* stage_r = (uint16_t*)(gbase + R);
+    __shared__ uint32_t warp_tot[BIN_THREADS / 32 + 1];
+
+    using W = typename C1::W;
+    SaltSrc<C1> ss;
+    ss.init(0, nullptr, nullptr);
+    const Params& p = bp.f;
+    const uint32_t tid = threadIdx.x;
+
+    for (uint64_t c = blockIdx.x; c * BIN_CHUNK < p.n; c += gridDim.x) {
+        const uint64_t base = c * BIN_CHUNK;
+        const uint32_t cnt = (uint32_t)min((uint64_t)BIN_CHUNK, p.n - base);
+        for (uint32_t r = tid; r < R; r += BIN_THREADS) hist[r] = 0;
+        __syncthreads();
+        // hash once per key; count per range (coalesced key loads: i*256+tid)
+        uint64_t rec[BIN_KPT];
+        uint32_t rl[BIN_KPT];
+#pragma unroll
+        for (int i = 0; i < BIN_KPT; ++i) {
+            const uint32_t li = i * BIN_THREADS + tid;
+            rl[i] = 0xFFFFFFFFu;
+            if (li < cnt) {
+                const uint64_t h = xxh64_u64(ld_key1(p.keys + base + li), p.seed);
+                const uint32_t blk = block_of(h, p.b32);
+                const uint32_t r = blk >> bp.lg_bpr;
+                rec[i] = ((uint64_t)blk << 32) | (uint32_t)h;
+                rl[i] = (r << 16) | atomicAdd(&hist[r], 1u);
+            }
+        }
+        __syncthreads();
+        // reserve this chunk's run in every touched bucket
+        for (uint32_t r = tid; r < R; r += BIN_THREADS)
+            gbase[r] = hist[r] ? atomicAdd(&bp.cursor[r], (unsigned long long)hist[r]) : 0ULL;
+        block_exclusive_scan<BIN_THREADS>(hist, R, warp_tot);  // hist -> run offsets in stage
+        // counting-sort the records by range in shared memory
+#pragma unroll
+        for (int i = 0; i < BIN_KPT; ++i) {
+            if (rl[i] != 0xFFFFFFFFu) {
+                const uint32_t r = rl[i] >> 16, pos = hist[r] + (rl[i] & 0xFFFFu);
+                stage[pos] = rec[i];
+                stage_r[pos] = (uint16_t)r;
+            }
+        }
+        __syncthreads();
+        // write the runs out (consecutive slots of a run -> consecutive addresses)
+        for (uint32_t j = tid; j < cnt; j += BIN_THREADS) {
+            const uint32_t r = stage_r[j];
+            const unsigned long long off = gbase[r] + (j - hist[r]);
+            const uint64_t v = stage[j];
+            if (off < bp.cap) {
+                bp.recs[(uint64_t)r * bp.cap + off] = v;
+            } else {  // bucket full: OR this key in directly (order-free)
+                add_part<C1>((W*)p.words, (uint32_t)v, (uint32_t)(v >> 32), 0, ss);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Phase 2: apply ONE bucket (bp.range) with the add schedule of C.  The host
+// launches the ranges one after another, so the whole GPU works inside one
+// L2-resident filter range at a time (a single grid-stride pass over all
+// buckets lets fast SMs drift several ranges ahead and the working set falls
+// out of L2: measured 10% RED hit rate vs ~90% expected).
+template <class C>
+__global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
+{
+    using W = typename C::W;
+    constexpr int KPT = C::KPT;
+    constexpr uint64_t TILE = 32 * KPT;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t pos = lane & (uint32_t)(C::THETA - 1);
+    const uint32_t gbase = lane & ~(uint32_t)(C::THETA - 1);
+    SaltSrc<C> ss;
+    ss.init(pos, nullptr, nullptr);
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    W* F = (W*)bp.f.words;
+    const uint64_t r = bp.range;
+    const uint64_t cnt = min((uint64_t)bp.cursor[r], bp.cap);
+    const uint64_t ntile = (cnt + TILE - 1) / TILE;
+    for (uint64_t lt = gw; lt < ntile; lt += nw) {
+        const uint64_t* rp = bp.recs + r * bp.cap + lt * TILE + (uint64_t)lane * KPT;
+        const uint64_t left = cnt - lt * TILE;
+        uint64_t rec[KPT];
+        bool valid[KPT];
+        if (left >= TILE) {
+            uint64_t k[KPT];
+            load_tile_keys<KPT>(rp, 0, true, k);
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) {
+                rec[j] = k[j];
+                valid[j] = true;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) {
+                valid[j] = (uint64_t)lane * KPT + j < left;
+                rec[j] = valid[j] ? ld_key1(rp + j) : 0ULL;
+            }
+        }
+        if constexpr (C::THETA == 1) {
+#pragma unroll
+            for (int j = 0; j < KPT; ++j)
+                if (valid[j]) add_part<C>(F, (uint32_t)rec[j], (uint32_t)(rec[j] >> 32), 0, ss);
+        } else {
+#pragma unroll 1
+            for (int rr = 0; rr < C::THETA; ++rr) {
+                const uint32_t src = gbase + rr;
+#pragma unroll
+                for (int j = 0; j < KPT; ++j) {
+                    const uint32_t l = __shfl_sync(0xffffffffu, (uint32_t)rec[j], src);
+                    const uint32_t bk = __shfl_sync(0xffffffffu, (uint32_t)(rec[j] >> 32), src);
+                    const bool v = __shfl_sync(0xffffffffu, (int)valid[j], src);
+                    if (v) add_part<C>(F, l, bk, pos, ss);
+                }
+            }
+        }
+    }
+}
+
+}  // namespace bf

@@ -149,20 +149,24 @@ __device__ __forceinline__ uint64_t ld_key1(const uint64_t* p)
 // Filter word loads of PHI contiguous S-bit words, the widest single load
 // per 32 bytes (LDG.256 on sm_100a; "vec_load_words").  The filter
 // is read-only during contains, so the non-coherent path is legal.
+// .L2::64B caps the L2 fill on a miss at 64 bytes: by default a random
+// 32-byte block miss on an HBM-resident filter fetches a whole 128-byte line
+// (ncu: 127 DRAM bytes per key), 4x the block; 64 B is the HBM access
+// granularity.  No effect while the filter is L2-resident.
 template <int S, int PHI> struct VecLoad;
 
 template <int PHI> struct VecLoad<64, PHI> {
     static __device__ __forceinline__ void run(const unsigned long long* p, unsigned long long* w)
     {
         if constexpr (PHI == 1) {
-            asm("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(w[0]) : "l"(p));
+            asm("ld.global.nc.L1::no_allocate.L2::64B.u64 %0, [%1];" : "=l"(w[0]) : "l"(p));
         } else if constexpr (PHI == 2) {
-            asm("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
+            asm("ld.global.nc.L1::no_allocate.L2::64B.v2.u64 {%0,%1}, [%2];"
                          : "=l"(w[0]), "=l"(w[1]) : "l"(p));
         } else {
 #pragma unroll
             for (int c = 0; c < PHI / 4; ++c)
-                asm("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                asm("ld.global.nc.L1::no_allocate.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];"
                              : "=l"(w[4 * c]), "=l"(w[4 * c + 1]), "=l"(w[4 * c + 2]), "=l"(w[4 * c + 3])
                              : "l"(p + 4 * c));
         }
@@ -173,17 +177,17 @@ template <int PHI> struct VecLoad<32, PHI> {
     static __device__ __forceinline__ void run(const uint32_t* p, uint32_t* w)
     {
         if constexpr (PHI == 1) {
-            asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(w[0]) : "l"(p));
+            asm("ld.global.nc.L1::no_allocate.L2::64B.u32 %0, [%1];" : "=r"(w[0]) : "l"(p));
         } else if constexpr (PHI == 2) {
-            asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+            asm("ld.global.nc.L1::no_allocate.L2::64B.v2.u32 {%0,%1}, [%2];"
                          : "=r"(w[0]), "=r"(w[1]) : "l"(p));
         } else if constexpr (PHI == 4) {
-            asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+            asm("ld.global.nc.L1::no_allocate.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];"
                          : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
         } else {
 #pragma unroll
             for (int c = 0; c < PHI / 8; ++c)
-                asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                asm("ld.global.nc.L1::no_allocate.L2::64B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                              : "=r"(w[8 * c]), "=r"(w[8 * c + 1]), "=r"(w[8 * c + 2]), "=r"(w[8 * c + 3]),
                                "=r"(w[8 * c + 4]), "=r"(w[8 * c + 5]), "=r"(w[8 * c + 6]), "=r"(w[8 * c + 7])
                              : "l"(p + 8 * c));

@@ -338,3 +338,76 @@ def test_large_filter_offsets_sampled(bflib, cuda):
     out = f.contains(_to_dev(torch, q, cuda))
     torch.cuda.synchronize()
     assert (out.cpu().numpy().view(np.uint32) == 0xFFFFFFFF).all()
+
+
+BINNED_CFGS = [(3, 256, 64, 8, 0), (1, 256, 64, 8, 0), (4, 256, 32, 8, 4), (2, 64, 64, 6, 0), (3, 256, 32, 16, 0)]
+
+
+@pytest.mark.parametrize("cfg", BINNED_CFGS)
+@pytest.mark.parametrize("range_bytes,batch", [(1 << 16, 0), (1 << 15, 30_000), (3 << 14, 7_777)])
+def test_binned_add_matches_oracle(bflib, cuda, cfg, range_bytes, batch):
+    """BF_ADD_BINNED (hash once, bin by filter range, apply range-major) builds
+    exactly the oracle's filter, across several ranges, batches and a ragged
+    last range."""
+    import torch
+    bf = bflib
+    v, B, S, k, z = cfg
+    m = (1 << 22) + 5 * B  # b not a power of two; last range partial
+    keys = synth.keys(321, 100_003)
+    o = OracleFilter(v, m, B=B, S=S, k=k, z=z)
+    o.add(keys)
+    f = bf.Filter(m, k, B, S, variant=v, z=z)
+    f.set_add_mode(bf.BF_ADD_BINNED, range_bytes, batch)
+    f.add(_to_dev(torch, keys, cuda))
+    torch.cuda.synchronize()
+    assert f.add_mode() == (bf.BF_ADD_BINNED, 1)
+    assert np.array_equal(_gpu_bytes(f), o.bytes())
+    q = np.concatenate([keys[:5000], synth.negatives(5000)])
+    assert np.array_equal(_gpu_contains(torch, f, _to_dev(torch, q, cuda)), o.contains(q))
+
+
+def test_binned_add_bucket_overflow(bflib, cuda):
+    """Keys concentrated in one range overflow its bucket; the overflow is
+    OR-ed in directly and the filter is still exact."""
+    import torch
+    bf = bflib
+    m, B = 1 << 22, 256
+    o_geom = OracleFilter(3, m, B=B, S=64, k=8, allocate=False)
+    cand = synth.keys(9, 200_000)
+    b = o_geom.b
+    per_range = (1 << 15) // (B // 8)
+    hot = np.array([key for key in cand if o_geom.pattern(int(key))[0] < per_range], dtype=np.uint64)
+    keys = np.concatenate([hot, cand[:20_000]])
+    assert hot.size > 4000 and b // per_range == 16
+    o = OracleFilter(3, m, B=B, S=64, k=8)
+    o.add(keys)
+    f = bf.Filter(m, 8, B, 64, "SBF")
+    f.set_add_mode(bf.BF_ADD_BINNED, 1 << 15, 0)
+    f.add(_to_dev(torch, keys, cuda))
+    torch.cuda.synchronize()
+    assert np.array_equal(_gpu_bytes(f), o.bytes())
+
+
+def test_binned_add_large_filter_sampled(bflib, cuda):
+    """Binned add on an 8 GiB filter (256 ranges of 32 MiB): sampled block
+    ranges equal the oracle's."""
+    import torch
+    bf = bflib
+    m, n = 1 << 36, 1 << 24
+    free, _ = torch.cuda.mem_get_info()
+    if free < (m // 8) + (1 << 31):
+        pytest.skip("not enough device memory")
+    kd = torch.empty(n, dtype=torch.int64, device=cuda)
+    bf.bf_keygen(kd, n, 77)
+    f = bf.Filter(m, 8, 256, 64, "SBF")
+    f.set_add_mode(bf.BF_ADD_BINNED)
+    f.add(kd)
+    torch.cuda.synchronize()
+    assert f.add_mode()[1] == 1
+    keys = synth.keys(77, n)
+    o = OracleFilter(3, m, B=256, S=64, k=8, allocate=False)
+    data = f.data()
+    for lo in (0, o.b // 3, o.b - 2048):
+        hi = lo + 2048
+        assert np.array_equal(data[lo * 32: hi * 32].cpu().numpy(),
+                              o.add_range(keys, lo, hi, threads=os.cpu_count())), lo
