@@ -81,28 +81,60 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock, power and throttle reasons sampled DURING the timed region
+    (NVML in-process every 5 ms; nvidia-smi as a fallback)."""
+    BITS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, index: int):
-        self.index = index
-        self.rows = []
+    def __init__(self, local_rank: int):
+        self.local_rank = local_rank
+        self.rows = []  # (sm_mhz, max_mhz, power_w, reasons set)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(local_rank)
+            try:
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(local_rank)
+            self._nvml = (pynvml, h)
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv, h = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        return (float(sm), float(mx), pw, {k for k, v in self.BITS.items() if bits & v})
+
+    def _sample_smi(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", f"--id={self.local_rank}", f"--query-gpu={q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip().split(",")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        return (float(out[0]), float(out[1]), float(out[2]),
+                {names[i] for i in range(4) if out[3 + i].strip() == "Active"})
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                self.rows.append(self._sample_nvml() if self._nvml else self._sample_smi())
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.005 if self._nvml else 0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -116,14 +148,11 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[4 + i]
-                          and not r[4 + i].startswith("Not")})
-        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(set().union(*(r[3] for r in self.rows))),
+                "samples": len(self.rows), "power_w_max": max(r[2] for r in self.rows),
+                "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 # --------------------------------------------------------------------- reference
@@ -280,6 +309,25 @@ def run_ours(a, cfg, rank, world, local_rank):
                 "note": ("L2-resident filter: HBM carries only keys/results, so this fraction is "
                          "bounded far below 1 by design; roofline_l2 is the random-access bound")
                 if cfg["residency"] == "L2" else "HBM-resident filter"}
+    # dram bytes per launch of this kernel from the committed ncu --set full
+    # capture of the same command (profiles/ncu_traffic.json), if present
+    try:
+        lay = f.layout(0 if dominant == "add" else 1)
+        vid = VARIANT_IDS[cfg["variant"]]
+        lgs = (cfg["B"] // cfg["S"]).bit_length() - 1
+        sig = (f"Cfg<{vid}, {cfg['S']}, {lgs}, {cfg['k']}, {cfg['z']}, {lay['theta']}, {lay['phi']}, "
+               f"{lay['kpt']}, {lay['hash_variant']}>, {1 if dominant == 'add' else 0}>")
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        hit = [v for k, v in tr["kernels"].items() if sig in k and v.get("n") == n]
+        if hit:
+            roofline["traffic"] = hit[0]["dram_bytes_per_launch"]
+            roofline["traffic_source"] = tr.get("source")
+    except Exception:
+        pass
+    if probe:
+        pk = probe["red"] if dominant == "add" else probe["read"]
+        roofline["probe_peak_gkeys_s"] = pk
+        roofline["probe_frac"] = round((n / (t_dom * 1e-3) / 1e9) / pk, 4)
     res = {
         "metric": "bulk add+contains throughput (configs[1], L2-resident, % of roofline)",
         "value": round(value, 3), "unit": "Gkeys/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,

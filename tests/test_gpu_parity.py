@@ -411,3 +411,37 @@ def test_binned_add_large_filter_sampled(bflib, cuda):
         hi = lo + 2048
         assert np.array_equal(data[lo * 32: hi * 32].cpu().numpy(),
                               o.add_range(keys, lo, hi, threads=os.cpu_count())), lo
+
+
+def _iso_rows():
+    import json
+    path = os.path.join(ROOT, "profiles", "iso_fpr_table.json")
+    return json.load(open(path))["c2"]["rows"]
+
+
+@pytest.mark.parametrize("row", _iso_rows(), ids=lambda r: f"v{r['variant']}_B{r['B']}_S{r['S']}_k{r['k']}_z{r['z']}")
+def test_iso_fpr_configs1_rows(bflib, cuda, row):
+    """configs[1] at iso FPR 1e-3 (32 MiB, n_iso keys from the exact model,
+    profiles/iso_fpr_table.json written by tools/make_iso_table.py from
+    oracle/ only): the GPU's measured FPR on 2^24 absent keys is within 4
+    binomial sigma of the exact ideal-hash model, and every inserted key is
+    found."""
+    import torch
+    bf = bflib
+    v, B, S, k, z = row["variant"], row["B"], row["S"], row["k"], row["z"]
+    m, n, Q = 1 << 28, row["n_iso"], 1 << 24
+    f = bf.Filter(m, k, B, S, variant=v, z=z)
+    keys = torch.empty(n, dtype=torch.int64, device=cuda)
+    bf.bf_keygen(keys, n, 0)
+    f.add(keys)
+    neg = torch.empty(Q, dtype=torch.int64, device=cuda)
+    bf.bf_keygen(neg, Q, synth.NEG_BASE)
+    out = f.contains(neg)
+    pos = f.contains(keys)
+    torch.cuda.synchronize()
+    fp = int(np.unpackbits(out.cpu().numpy().view(np.uint8)).sum())
+    p = row["fpr_model"]
+    zz = (fp - Q * p) / np.sqrt(Q * p * (1 - p))
+    assert abs(zz) <= 4.0, (fp, Q * p)
+    got = np.unpackbits(pos.cpu().numpy().view(np.uint8), bitorder="little")[:n]
+    assert got.all()

@@ -1,0 +1,72 @@
+#!/usr/bin/env python
+"""Write profiles/iso_fpr_table.json: for every configs[1] sweep row (and the
+configs[2]/[3] variants) the bits-per-key c_iso at the target FPR and the
+exact-model FPR at the resulting load, from the oracle's exact ideal-hash
+model (oracle/fpr_model.py).  Stored expected values come
+only from this script, which calls only oracle/.
+
+    python tools/make_iso_table.py
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import fpr_model as M  # noqa: E402
+
+BBF, RBBF, SBF, CSBF = 1, 2, 3, 4
+ROWS = [(RBBF, 32, 32, 0), (RBBF, 64, 64, 0), (SBF, 64, 32, 0), (SBF, 128, 64, 0),
+        (SBF, 128, 32, 0), (SBF, 256, 64, 0), (SBF, 256, 32, 0), (BBF, 128, 64, 0),
+        (BBF, 256, 64, 0), (CSBF, 256, 32, 2), (CSBF, 256, 32, 4), (CSBF, 256, 64, 2)]
+
+
+def valid(v, B, S, k, z):
+    s = B // S
+    return not ((v == SBF and k % s) or (v == CSBF and k % z))
+
+
+def n_iso(v, B, S, k, z, m_bits, target):
+    """Largest n with exact-model FPR <= target (bisection on n)."""
+    b = m_bits // B
+    lo, hi = 1, m_bits // 2
+    while hi - lo > max(1, lo // 20000):
+        mid = (lo + hi) // 2
+        if M.fpr_exact(v, mid, b, B, S, k, z) <= target:
+            lo = mid
+        else:
+            hi = mid
+    return lo
+
+
+def main():
+    out = {"_source": "tools/make_iso_table.py (oracle/fpr_model.py exact ideal-hash model)",
+           "c2": {"m_bits": 1 << 28, "target_fpr": 1e-3, "rows": []}}
+    m = 1 << 28
+    for v, B, S, z in ROWS:
+        for k in range(4, 17):
+            if not valid(v, B, S, k, z):
+                continue
+            n = n_iso(v, B, S, k, z, m, 1e-3)
+            f = M.fpr_exact(v, n, m // B, B, S, k, z)
+            out["c2"]["rows"].append({"variant": v, "B": B, "S": S, "k": k, "z": z, "n_iso": n,
+                                      "c_iso": m / n, "fpr_model": f,
+                                      "fill_model": M.fill_exact(v, n, m // B, B, S, k, z)})
+            print(v, B, S, k, z, n, round(m / n, 2), f, flush=True)
+    # configs[3]: SBF 256/32 at FPR 1e-4, c_iso for a large filter (b = 2^20 blocks)
+    out["c4"] = {"target_fpr": 1e-4, "rows": []}
+    for k in (8, 16):
+        n = n_iso(SBF, 256, 32, k, 0, 256 << 20, 1e-4)
+        out["c4"]["rows"].append({"variant": SBF, "B": 256, "S": 32, "k": k, "z": 0,
+                                  "c_iso": (256 << 20) / n})
+        print("c4", k, (256 << 20) / n, flush=True)
+    path = os.path.join(ROOT, "profiles", "iso_fpr_table.json")
+    json.dump(out, open(path, "w"), indent=1)
+    print("wrote", path)
+
+
+if __name__ == "__main__":
+    main()

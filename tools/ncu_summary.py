@@ -79,5 +79,29 @@ def full(path):
         print()
 
 
+def traffic(path, n_keys, out_json):
+    """profiles/ncu_traffic.json: dram read+write bytes per launch per kernel
+    (the `traffic` field of bench.py's roofline object)."""
+    import json
+    import os
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h = rows[0]
+    acc = defaultdict(list)
+    for r in rows[2:]:
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        b = float(r[h.index("dram__bytes_read.sum")].replace(",", "")) * scale[rows[1][h.index("dram__bytes_read.sum")]] + \
+            float(r[h.index("dram__bytes_write.sum")].replace(",", "")) * scale[rows[1][h.index("dram__bytes_write.sum")]]
+        acc[r[h.index("Kernel Name")]].append(b)
+    old = json.load(open(out_json)) if os.path.exists(out_json) else {"kernels": {}}
+    old["source"] = f"ncu --set full capture {os.path.basename(path)} (dram__bytes_read.sum + dram__bytes_write.sum per launch)"
+    for k, v in acc.items():
+        old["kernels"][k] = {"dram_bytes_per_launch": sum(v) / len(v), "n": int(n_keys), "capture": os.path.basename(path)}
+    json.dump(old, open(out_json, "w"), indent=1)
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    if sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4])
+    else:
+        {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])

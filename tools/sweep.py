@@ -33,24 +33,19 @@ def instances():
     return g.instances()
 
 
-def c_iso(variant, B, S, k, z, fpr=1e-4):
-    """bits/key at the target FPR from the exact model (oracle/fpr_model)."""
-    from oracle import fpr_model as M
-    lo, hi = 4.0, 200.0
-    b = 1 << 20
-    for _ in range(50):
-        c = (lo + hi) / 2
-        n = int(b * B / c)
-        if M.fpr_exact(variant, n, b, B, S, k, z) > fpr:
-            lo = c
-        else:
-            hi = c
-    return hi
+def c_iso(variant, B, S, k, z):
+    """bits/key at FPR 1e-4 (profiles/iso_fpr_table.json, written from the
+    exact model by tools/make_iso_table.py)."""
+    tab = json.load(open(os.path.join(ROOT, "profiles", "iso_fpr_table.json")))["c4"]["rows"]
+    for r in tab:
+        if (r["variant"], r["B"], r["S"], r["k"], r["z"]) == (variant, B, S, k, z):
+            return r["c_iso"]
+    raise KeyError((variant, B, S, k, z))
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--set", default="c2", choices=["c2", "c4", "c4l2", "one"])
+    ap.add_argument("--set", default="c2", choices=["c2", "c2iso", "c4", "c4l2", "one"])
     ap.add_argument("--n", type=int, default=1 << 26)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cfg", default=None, help="v,B,S,k,z for --set one")
@@ -62,6 +57,8 @@ def main():
     from paper_2512_15595_b200 import bf
 
     dev = torch.device("cuda:0")
+    if a.set == "c2iso":
+        return iso_sweep(a, torch, bf, dev)
     inst = instances()
     groups = defaultdict(list)
     for op, v, B, S, k, z, th, ph, kpt, hv in inst:
@@ -127,6 +124,56 @@ def main():
         if n % 32 == 0:
             assert int((out != -1).sum()) == 0, f"false negatives in {cfg}"
         del f
+
+
+def iso_sweep(a, torch, bf, dev):
+    """configs[1] at iso FPR 1e-3: per row, add n_iso keys (profiles/
+    iso_fpr_table.json) into a cleared 32 MiB filter, query 2^26 absent keys;
+    report both throughputs and the measured FPR against the exact model."""
+    import math
+
+    import numpy as np
+
+    import synth
+    tab = json.load(open(os.path.join(ROOT, "profiles", "iso_fpr_table.json")))["c2"]
+    m, Q = tab["m_bits"], 1 << 26
+    neg = torch.empty(Q, dtype=torch.int64, device=dev)
+    bf.bf_keygen(neg, Q, synth.NEG_BASE)
+    out = torch.empty(Q // 32, dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fh = open(a.out, "a") if a.out else None
+    for row in tab["rows"]:
+        v, B, S, k, z, n = row["variant"], row["B"], row["S"], row["k"], row["z"], row["n_iso"]
+        keys = torch.empty(n, dtype=torch.int64, device=dev)
+        bf.bf_keygen(keys, n, 0)
+        f = bf.Filter(m, k, B, S, v, z=z)
+        ta, tc = [], []
+        for r in range(a.reps + 1):
+            f.clear()
+            e0.record(st)
+            f.add(keys)
+            e1.record(st)
+            torch.cuda.synchronize()
+            if r:
+                ta.append(e0.elapsed_time(e1))
+            e0.record(st)
+            f.contains(neg, out)
+            e1.record(st)
+            torch.cuda.synchronize()
+            if r:
+                tc.append(e0.elapsed_time(e1))
+        fp = int(np.unpackbits(out.cpu().numpy().view(np.uint8)).sum())
+        p = row["fpr_model"]
+        rec = {"set": "c2iso", "variant": v, "B": B, "S": S, "k": k, "z": z, "m_bits": m, "n_iso": n,
+               "c_iso": round(row["c_iso"], 3), "add_gkeys_s": round(n / statistics.median(ta) / 1e6, 3),
+               "contains_gkeys_s": round(Q / statistics.median(tc) / 1e6, 3), "fpr": fp / Q,
+               "fpr_model": p, "fpr_z": round((fp - Q * p) / math.sqrt(Q * p * (1 - p)), 2),
+               "layout_add": f.layout(0), "layout_contains": f.layout(1)}
+        print(json.dumps(rec), flush=True)
+        if fh:
+            fh.write(json.dumps(rec) + "\n")
+        del f, keys
 
 
 if __name__ == "__main__":
