@@ -91,7 +91,7 @@ def test_every_compiled_schedule_matches_oracle(bflib, cuda, cfg, scheds):
 
 
 GENERIC = [  # no specialized instantiation -> generic runtime kernel
-    (3, 512, 64, 16, 0), (3, 1024, 64, 16, 0), (4, 1024, 64, 16, 4), (1, 512, 32, 20, 0),
+    (3, 512, 32, 16, 0), (3, 1024, 32, 32, 0), (4, 1024, 32, 16, 4), (1, 512, 32, 20, 0),
     (3, 256, 64, 20, 0), (2, 64, 64, 25, 0), (4, 512, 32, 16, 8), (1, 32, 32, 3, 0),
     (3, 128, 32, 32, 0), (4, 256, 64, 8, 1),
 ]

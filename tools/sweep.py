@@ -45,7 +45,7 @@ def c_iso(variant, B, S, k, z):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--set", default="c2", choices=["c2", "c2iso", "c4", "c4l2", "one"])
+    ap.add_argument("--set", default="c2", choices=["c2", "c2iso", "c4", "c4l2", "one", "paper"])
     ap.add_argument("--n", type=int, default=1 << 26)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cfg", default=None, help="v,B,S,k,z for --set one")
@@ -59,6 +59,8 @@ def main():
     dev = torch.device("cuda:0")
     if a.set == "c2iso":
         return iso_sweep(a, torch, bf, dev)
+    if a.set == "paper":
+        return paper_tables(a, torch, bf, dev)
     inst = instances()
     groups = defaultdict(list)
     for op, v, B, S, k, z, th, ph, kpt, hv in inst:
@@ -124,6 +126,90 @@ def main():
         if n % 32 == 0:
             assert int((out != -1).sum()) == 0, f"false negatives in {cfg}"
         del f
+
+
+# the paper's Table 1 (1 GB) and Table 2 (32 MB), G keys/s
+PAPER = {
+    ("1GB", "contains"): {64: [48.69], 128: [48.54, 44.62], 256: [47.79, 43.74, 41.64],
+                          512: [25.35, 40.66, 40.15, 33.66], 1024: [12.81, 36.01, 36.96, 33.38, 24.54]},
+    ("1GB", "add"): {64: [22.43], 128: [13.57, 22.26], 256: [7.59, 13.65, 22.10],
+                     512: [4.58, 7.72, 15.31, 20.75], 1024: [2.88, 5.02, 8.53, 15.41, 15.61]},
+    ("32MB", "contains"): {64: [155.89], 128: [149.50, 51.58], 256: [141.88, 51.57, 50.40],
+                           512: [104.55, 50.20, 50.35, 45.34], 1024: [44.87, 48.95, 48.69, 45.22, 42.11]},
+    ("32MB", "add"): {64: [125.19], 128: [66.07, 121.45], 256: [33.91, 63.25, 111.88],
+                      512: [17.10, 20.67, 35.56, 72.41], 1024: [8.19, 10.37, 11.55, 18.91, 39.22]},
+}
+
+
+def paper_tables(a, torch, bf, dev):
+    """The paper's layout tables on this B200: SBF, S=64, k=16, B = 64..1024
+    (B=64 is the RBBF), every Θ with Φ = s/Θ (KPT: best of 1/2/4), a 32 MiB
+    (L2) and a 1 GiB (HBM) filter; add uses the paper's direct method (plus
+    one binned row at 1 GiB)."""
+    n = a.n
+    keys = torch.empty(n, dtype=torch.int64, device=dev)
+    bf.bf_keygen(keys, n, 0)
+    out = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fh = open(a.out, "a") if a.out else None
+
+    def timeit(fn, reps, pre=None):
+        ts = []
+        for r in range(reps + 1):
+            if pre:
+                pre()
+            e0.record(st)
+            fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            if r:
+                ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    for size, m in (("32MB", 1 << 28), ("1GB", 1 << 33)):
+        for B in (64, 128, 256, 512, 1024):
+            s = B // 64
+            v = 2 if B == 64 else 3
+            f = bf.Filter(m, 16, B, 64, v)
+            for op in ("add", "contains"):
+                for ti, th in enumerate([1 << i for i in range(s.bit_length())]):
+                    best = None
+                    for kpt in (1, 2, 4):
+                        try:
+                            f.set_layout(0 if op == "add" else 1, th, s // th, kpt, 0)
+                        except bf.BFError:
+                            continue
+                        if op == "add":
+                            f.set_add_mode(bf.BF_ADD_DIRECT)
+                            t = timeit(lambda: f.add(keys), a.reps, pre=f.clear)
+                        else:
+                            f.set_add_mode(bf.BF_ADD_DIRECT)
+                            f.clear()
+                            f.add(keys)
+                            t = timeit(lambda: f.contains(keys, out), a.reps)
+                        g = n / (t * 1e-3) / 1e9
+                        if best is None or g > best[0]:
+                            best = (g, kpt)
+                    if best is None:
+                        continue
+                    rec = {"set": "paper", "size": size, "m_bits": m, "B": B, "S": 64, "k": 16, "op": op,
+                           "theta": th, "phi": s // th, "kpt": best[1], "gkeys_s": round(best[0], 2),
+                           "paper_gkeys_s": PAPER[(size, op)][B][ti], "n": n}
+                    print(json.dumps(rec), flush=True)
+                    if fh:
+                        fh.write(json.dumps(rec) + "\n")
+            if size == "1GB":
+                f.set_layout(0, 0, 0)
+                f.set_add_mode(bf.BF_ADD_BINNED)
+                t = timeit(lambda: f.add(keys), a.reps, pre=f.clear)
+                rec = {"set": "paper", "size": size, "m_bits": m, "B": B, "S": 64, "k": 16, "op": "add_binned",
+                       "theta": f.layout(0)["theta"], "phi": f.layout(0)["phi"], "kpt": f.layout(0)["kpt"],
+                       "gkeys_s": round(n / (t * 1e-3) / 1e9, 2), "n": n}
+                print(json.dumps(rec), flush=True)
+                if fh:
+                    fh.write(json.dumps(rec) + "\n")
+            del f
 
 
 def iso_sweep(a, torch, bf, dev):
