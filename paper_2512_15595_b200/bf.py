@@ -223,8 +223,11 @@ class Filter:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h:
-            bf_destroy(h)
+        if h and _lib is not None:  # module globals may already be gone at interpreter exit
+            try:
+                _lib.bf_destroy(h)
+            except Exception:
+                pass
             self.handle = None
 
     def add(self, keys, stream=None):

@@ -142,7 +142,13 @@ struct bf_filter {
 static int validate(uint64_t m_bits, uint32_t k, uint32_t B, uint32_t S, uint32_t variant, uint32_t* z_out)
 {
     const uint32_t v = variant & 0xFF, z = (variant >> 8) & 0xFF;
-    if (v == BF_CBF) return fail(BF_EUNSUPPORTED, "BF_CBF is oracle-only (no GPU kernel in this build)");
+    if (v == BF_CBF) {  // classical filter: k positions over m <= 2^32 bits
+        if (variant >> 8) return fail(BF_EINVAL, "unknown variant bits 0x%x", variant);
+        if (k < 1 || k > 32) return fail(BF_EINVAL, "k must be in 1..32 (got %u)", k);
+        if (m_bits < 1 || m_bits > (1ULL << 32)) return fail(BF_EINVAL, "CBF needs 1 <= m_bits <= 2^32");
+        *z_out = 0;
+        return BF_OK;
+    }
     if (v != BF_BBF && v != BF_RBBF && v != BF_SBF && v != BF_CSBF) return fail(BF_EINVAL, "unknown variant %u", v);
     if (variant >> 16) return fail(BF_EINVAL, "unknown variant bits 0x%x", variant);
     if (S != 32 && S != 64) return fail(BF_EINVAL, "word_bits must be 32 or 64 (got %u)", S);
@@ -186,9 +192,10 @@ static int set_sched(bf_filter* f, int op, int theta, int phi, int kpt, int hv)
     if (hv < 0 || hv > 3) return fail(BF_EINVAL, "hash_variant must be 0..3");
     InstKey key{(uint8_t)op, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z,
                 (uint8_t)theta, (uint8_t)phi, (uint8_t)kpt, (uint8_t)hv};
-    KernelFn fn = registry_find(key);
+    KernelFn fn = f->variant == BF_CBF ? nullptr : registry_find(key);
     Sched sc{theta, phi, kpt, hv, fn, fn != nullptr, 0};
-    if (!fn) {
+    if (f->variant == BF_CBF) sc = Sched{1, 1, 1, 0, cbf_entry(op == 0, (int)f->k), false, 0};
+    if (!fn && f->variant != BF_CBF) {
         // no specialized instantiation (bf_set_layout refuses explicit
         // requests for uncompiled schedules before getting here): the
         // generic runtime-parameter kernel, Θ = 1, one key per thread
@@ -229,6 +236,9 @@ bf_filter* bf_create_seeded(uint64_t m_bits, uint32_t k, uint32_t block_bits, ui
     f->variant = variant & 0xFF;
     f->z = z;
     f->k = k;
+    if (f->variant == BF_CBF) {  // one "block" per 32-bit word; positions span all m bits
+        block_bits = word_bits = 32;
+    }
     f->B = block_bits;
     f->S = word_bits;
     f->s = block_bits / word_bits;
@@ -343,7 +353,7 @@ static Params make_params(const bf_filter* f, const uint64_t* keys, uint64_t n, 
 {
     Params p;
     p.words = f->words;
-    p.b = f->b;
+    p.b = f->variant == BF_CBF ? f->m_bits : f->b;  // CBF kernels take m (bits)
     p.b32 = (uint32_t)f->b;
     p.keys = keys;
     p.n = n;

@@ -89,7 +89,7 @@ __device__ __forceinline__ uint64_t xxh64_u64(uint64_t key, uint64_t seed)
 }
 
 // SplitMix64 output function (synthetic key generator).
-__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x)
+__host__ __device__ constexpr uint64_t mix64(uint64_t x)
 {
     uint64_t z = x + 0x9E3779B97F4A7C15ULL;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;

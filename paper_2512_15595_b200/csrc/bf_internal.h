@@ -28,6 +28,7 @@ KernelFn registry_find(const InstKey& key);
 uint64_t registry_size();
 
 KernelFn generic_entry(int S, bool add);
+KernelFn cbf_entry(bool add, int k);
 void launch_keygen(uint64_t* out, uint64_t n, uint64_t base, cudaStream_t st, int grid);
 void launch_or_fold(void* dst, const void* srcs, uint32_t nsrc, uint64_t stride, uint64_t bytes,
                     cudaStream_t st, int grid);

@@ -33,7 +33,7 @@ def test_sass_has_256bit_loads_and_red_or(bflib):
 
 def test_validation_without_gpu(bflib):
     """Invalid configurations are rejected synchronously (BF_EINVAL) before any
-    CUDA call; CBF is BF_EUNSUPPORTED."""
+    CUDA call."""
     bf = bflib
     with pytest.raises(bf.BFError) as e:
         bf.bf_create(1 << 20, 10, 256, 64, bf.BF_SBF)  # k % s != 0
@@ -48,8 +48,8 @@ def test_validation_without_gpu(bflib):
         bf.bf_create(1 << 20, 6, 256, 32, bf.BF_CSBF_Z(4))  # k % z != 0
     assert e.value.code == bf.BF_EINVAL
     with pytest.raises(bf.BFError) as e:
-        bf.bf_create(1 << 20, 8, 256, 64, bf.BF_CBF)
-    assert e.value.code == bf.BF_EUNSUPPORTED
+        bf.bf_create((1 << 32) + 1, 8, 256, 64, bf.BF_CBF)  # CBF positions need m <= 2^32
+    assert e.value.code == bf.BF_EINVAL
     with pytest.raises(bf.BFError) as e:
         bf.bf_create(1 << 20, 0, 256, 64, bf.BF_BBF)
     assert e.value.code == bf.BF_EINVAL

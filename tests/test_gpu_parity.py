@@ -445,3 +445,23 @@ def test_iso_fpr_configs1_rows(bflib, cuda, row):
     assert abs(zz) <= 4.0, (fp, Q * p)
     got = np.unpackbits(pos.cpu().numpy().view(np.uint8), bitorder="little")[:n]
     assert got.all()
+
+
+@pytest.mark.parametrize("m,k", [(1 << 20, 7), ((1 << 22) + 13, 16), (1 << 25, 16), (999_983, 1), (1 << 32, 4)])
+def test_cbf_matches_oracle(bflib, cuda, m, k):
+    """GPU classical Bloom filter (NEXT N3; the paper's GPU CBF baseline,
+    P:L352/P:L392) == the oracle's CBF, bits and results, incl. m = 2^32."""
+    import torch
+    bf = bflib
+    keys = synth.keys(5, 70_001)
+    q = np.concatenate([keys[::3], synth.negatives(30_000)])
+    o = OracleFilter(0, m, k=k)
+    o.add(keys, threads=4)
+    f = bf.Filter(m, k, 256, 64, bf.BF_CBF)
+    assert f.layout(0)["specialized"] == 0
+    f.add(_to_dev(torch, keys, cuda))
+    torch.cuda.synchronize()
+    got = _gpu_bytes(f)
+    want = o.bytes()
+    assert np.array_equal(got[:want.size], want) and not got[want.size:].any()
+    assert np.array_equal(_gpu_contains(torch, f, _to_dev(torch, q, cuda)), o.contains(q, threads=4))
