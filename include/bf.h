@@ -158,6 +158,41 @@ int bf_get_add_mode(const bf_filter* f, int* mode, int* last_binned);
 int bf_get_layout(const bf_filter* f, int op, int* theta, int* phi, int* kpt,
                   int* hash_variant, int* specialized);
 
+/* ---- Block-range partitioned filters (filters larger than one GPU; NEXT
+ * N1 of SURVEY 8(f)).  A filter of b = ceil(m/B) blocks is split over nparts
+ * owners; owner p holds global blocks [floor(p*b/P), floor((p+1)*b/P)).  Keys
+ * are ROUTED to the owner of their block (hash once, bin by owner), the
+ * buckets travel with a fixed-count all-to-all (cap records per peer; NCCL
+ * all_to_all_single), and each owner applies / tests the records it
+ * receives.  The union of the parts is bit-identical to the unpartitioned
+ * filter.  Records are uint64 (global block << 32 | low hash half).
+ *
+ * bf_create_part: the local part `part` of such a filter (same arguments as
+ *   bf_create_seeded).  bf_geometry reports the GLOBAL b; bf_data the local
+ *   bytes.  bf_add / bf_contains on a part with nparts > 1 return BF_EINVAL. */
+bf_filter* bf_create_part(uint64_t m_bits, uint32_t k, uint32_t block_bits, uint32_t word_bits,
+                          uint32_t variant, uint64_t seed, uint32_t nparts, uint32_t part);
+int bf_part_info(const bf_filter* f, uint32_t* nparts, uint32_t* part, uint64_t* blk_lo,
+                 uint64_t* blk_hi, uint64_t* b_global);
+/* Route n device keys: record of key i goes to bucket owner(i) at
+ * recs[owner*cap + slot]; counts[owner] (device, zeroed here) receives the
+ * bucket sizes.  idx (nullable, same layout) receives idx_base + i, for
+ * contains.  A count above cap means records were dropped: the caller must
+ * retry with a larger cap (cap: a multiple of 128). */
+int bf_route(const bf_filter* f, const uint64_t* keys, uint64_t n, uint64_t idx_base,
+             uint64_t* recs, uint64_t* idx, uint64_t cap, unsigned long long* counts, void* stream);
+/* OR the routed records of nsrc source buckets (recs[s*cap ..], counts[s])
+ * into this part. */
+int bf_add_routed(bf_filter* f, const uint64_t* recs, const unsigned long long* counts,
+                  uint32_t nsrc, uint64_t cap, void* stream);
+/* Test routed records against this part: res[s*cap + j] = 1 / 0. */
+int bf_contains_routed(const bf_filter* f, const uint64_t* recs, const unsigned long long* counts,
+                       uint32_t nsrc, uint64_t cap, uint8_t* res, void* stream);
+/* out_bits[idx/32] |= 1 << idx%32 for every record with res == 1 (out_bits
+ * must be zeroed by the caller; atomic, any order). */
+int bf_scatter_results(const uint64_t* idx, const uint8_t* res, const unsigned long long* counts,
+                       uint32_t nsrc, uint64_t cap, uint32_t* out_bits, void* stream);
+
 /* dst[i] = OR over r < nsrc of src_r[i], for `bytes` bytes (multiple of 8).
  * srcs: device pointer to nsrc arrays laid out src_stride_bytes apart (the
  * receive buffer of an all-gather); dst may alias src_0.  The merge step of a

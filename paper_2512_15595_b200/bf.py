@@ -55,6 +55,13 @@ _SIGS = {
     "bf_probe_rng": (_i32, [_vp, _u64, _u32, _i32, _u32, _u64, _vp]),
     "bf_set_add_mode": (_i32, [_vp, _i32, _u64, _u64]),
     "bf_get_add_mode": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
+    "bf_create_part": (_vp, [_u64, _u32, _u32, _u32, _u32, _u64, _u32, _u32]),
+    "bf_part_info": (_i32, [_vp, C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u64), C.POINTER(_u64),
+                            C.POINTER(_u64)]),
+    "bf_route": (_i32, [_vp, _vp, _u64, _u64, _vp, _vp, _u64, _vp, _vp]),
+    "bf_add_routed": (_i32, [_vp, _vp, _vp, _u32, _u64, _vp]),
+    "bf_contains_routed": (_i32, [_vp, _vp, _vp, _u32, _u64, _vp, _vp]),
+    "bf_scatter_results": (_i32, [_vp, _vp, _vp, _u32, _u64, _vp, _vp]),
     "bf_launch_count": (_u64, []),
     "bf_last_error": (C.c_char_p, [C.POINTER(_i32)]),
     "bf_version": (C.c_char_p, []),
@@ -194,6 +201,40 @@ def bf_probe_red(buf, b: int, block_bits: int, lanes: int, keys, n: int | None =
 
 def bf_probe_rng(buf, b: int, block_bits: int, red: int, lanes: int, n: int, stream=None) -> None:
     _check(_lib.bf_probe_rng(_ptr(buf), b, block_bits, red, lanes, n, _stream(stream)))
+
+
+def bf_create_part(m_bits: int, k: int, block_bits: int, word_bits: int, variant: int, seed: int,
+                   nparts: int, part: int) -> int:
+    h = _lib.bf_create_part(m_bits, k, block_bits, word_bits, variant, seed, nparts, part)
+    if not h:
+        code, msg = last_error()
+        raise BFError(code, msg)
+    return h
+
+
+def bf_part_info(f: int) -> dict:
+    a, b = _u32(), _u32()
+    lo, hi, bg = _u64(), _u64(), _u64()
+    _check(_lib.bf_part_info(f, C.byref(a), C.byref(b), C.byref(lo), C.byref(hi), C.byref(bg)))
+    return dict(nparts=int(a.value), part=int(b.value), blk_lo=int(lo.value), blk_hi=int(hi.value),
+                b_global=int(bg.value))
+
+
+def bf_route(f: int, keys, n: int, idx_base: int, recs, idx, cap: int, counts, stream=None) -> None:
+    _check(_lib.bf_route(f, _ptr(keys), n, idx_base, _ptr(recs), _ptr(idx) if idx is not None else None,
+                         cap, _ptr(counts), _stream(stream)))
+
+
+def bf_add_routed(f: int, recs, counts, nsrc: int, cap: int, stream=None) -> None:
+    _check(_lib.bf_add_routed(f, _ptr(recs), _ptr(counts), nsrc, cap, _stream(stream)))
+
+
+def bf_contains_routed(f: int, recs, counts, nsrc: int, cap: int, res, stream=None) -> None:
+    _check(_lib.bf_contains_routed(f, _ptr(recs), _ptr(counts), nsrc, cap, _ptr(res), _stream(stream)))
+
+
+def bf_scatter_results(idx, res, counts, nsrc: int, cap: int, out_bits, stream=None) -> None:
+    _check(_lib.bf_scatter_results(_ptr(idx), _ptr(res), _ptr(counts), nsrc, cap, _ptr(out_bits), _stream(stream)))
 
 
 def bf_launch_count() -> int:

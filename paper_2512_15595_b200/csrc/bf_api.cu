@@ -137,6 +137,11 @@ struct bf_filter {
     uint64_t recs_bytes;
     unsigned long long* cursor;
     uint32_t cursor_n;
+    // block-range partition (NEXT N1): this filter holds global blocks
+    // [blk_lo, blk_hi) of a b_global-block filter split over nparts owners
+    uint32_t nparts, part;
+    uint64_t b_global, blk_lo, blk_hi;
+    uint32_t* bounds;  // device: nparts + 1 block boundaries
 };
 
 static int validate(uint64_t m_bits, uint32_t k, uint32_t B, uint32_t S, uint32_t variant, uint32_t* z_out)
@@ -218,11 +223,19 @@ const char* bf_last_error(int* code)
 
 uint64_t bf_launch_count(void) { return g_launches.load(); }
 
-bf_filter* bf_create_seeded(uint64_t m_bits, uint32_t k, uint32_t block_bits, uint32_t word_bits, uint32_t variant,
-                            uint64_t seed)
+static bf_filter* create_impl(uint64_t m_bits, uint32_t k, uint32_t block_bits, uint32_t word_bits, uint32_t variant,
+                              uint64_t seed, uint32_t nparts, uint32_t part)
 {
     uint32_t z = 0;
     if (validate(m_bits, k, block_bits, word_bits, variant, &z) != BF_OK) return nullptr;
+    if (nparts < 1 || nparts > 4096 || part >= nparts) {
+        fail(BF_EINVAL, "bad partition (nparts=%u part=%u; 1 <= nparts <= 4096)", nparts, part);
+        return nullptr;
+    }
+    if (nparts > 1 && ((variant & 0xFF) == BF_CBF || (m_bits + block_bits - 1) / block_bits < nparts)) {
+        fail(BF_EINVAL, "block-range partitions need a blocked variant with at least nparts blocks");
+        return nullptr;
+    }
     bf_filter* f = new (std::nothrow) bf_filter();
     if (!f) {
         fail(BF_ENOMEM, "host allocation failed");
@@ -244,7 +257,12 @@ bf_filter* bf_create_seeded(uint64_t m_bits, uint32_t k, uint32_t block_bits, ui
     f->s = block_bits / word_bits;
     f->m_bits = m_bits;
     f->b = (m_bits + block_bits - 1) / block_bits;
-    f->bytes = f->b * block_bits / 8;
+    f->nparts = nparts;
+    f->part = part;
+    f->b_global = f->b;
+    f->blk_lo = f->b * part / nparts;
+    f->blk_hi = f->b * (part + 1) / nparts;
+    f->bytes = (f->blk_hi - f->blk_lo) * block_bits / 8;
     f->seed = seed;
     cudaError_t e = cudaMalloc(&f->words, f->bytes);
     if (e != cudaSuccess) {
@@ -261,8 +279,21 @@ bf_filter* bf_create_seeded(uint64_t m_bits, uint32_t k, uint32_t block_bits, ui
         cuda_fail(e, "cudaMemset");
         return nullptr;
     }
+    if (nparts > 1) {
+        uint32_t hb[4097];
+        for (uint32_t p = 0; p <= nparts; ++p) hb[p] = (uint32_t)(f->b * p / nparts);  // b <= 2^32: hb[P] may wrap only if b == 2^32
+        e = cudaMalloc(&f->bounds, (nparts + 1) * sizeof(uint32_t));
+        if (e == cudaSuccess) e = cudaMemcpy(f->bounds, hb, (nparts + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(f->words);
+            delete f;
+            cuda_fail(e, "partition bounds");
+            return nullptr;
+        }
+    }
     if (set_sched(f, 0, 0, 0, 0, 0) != BF_OK || set_sched(f, 1, 0, 0, 0, 0) != BF_OK) {
         cudaFree(f->words);
+        if (f->bounds) cudaFree(f->bounds);
         delete f;
         return nullptr;
     }
@@ -271,9 +302,33 @@ bf_filter* bf_create_seeded(uint64_t m_bits, uint32_t k, uint32_t block_bits, ui
     return f;
 }
 
+bf_filter* bf_create_seeded(uint64_t m_bits, uint32_t k, uint32_t block_bits, uint32_t word_bits, uint32_t variant,
+                            uint64_t seed)
+{
+    return create_impl(m_bits, k, block_bits, word_bits, variant, seed, 1, 0);
+}
+
 bf_filter* bf_create(uint64_t m_bits, uint32_t k, uint32_t block_bits, uint32_t word_bits, uint32_t variant)
 {
-    return bf_create_seeded(m_bits, k, block_bits, word_bits, variant, 0);
+    return create_impl(m_bits, k, block_bits, word_bits, variant, 0, 1, 0);
+}
+
+bf_filter* bf_create_part(uint64_t m_bits, uint32_t k, uint32_t block_bits, uint32_t word_bits, uint32_t variant,
+                          uint64_t seed, uint32_t nparts, uint32_t part)
+{
+    return create_impl(m_bits, k, block_bits, word_bits, variant, seed, nparts, part);
+}
+
+int bf_part_info(const bf_filter* f, uint32_t* nparts, uint32_t* part, uint64_t* blk_lo, uint64_t* blk_hi,
+                 uint64_t* b_global)
+{
+    if (!f) return fail(BF_EINVAL, "null filter");
+    if (nparts) *nparts = f->nparts;
+    if (part) *part = f->part;
+    if (blk_lo) *blk_lo = f->blk_lo;
+    if (blk_hi) *blk_hi = f->blk_hi;
+    if (b_global) *b_global = f->b_global;
+    return BF_OK;
 }
 
 static void free_staging(bf_filter* f)
@@ -299,6 +354,7 @@ void bf_destroy(bf_filter* f)
     free_staging(f);
     if (f->recs) cudaFree(f->recs);
     if (f->cursor) cudaFree(f->cursor);
+    if (f->bounds) cudaFree(f->bounds);
     cudaFree(f->words);
     delete f;
 }
@@ -449,6 +505,7 @@ static int binned_add(bf_filter* f, const uint64_t* keys, uint64_t n, cudaStream
     for (uint64_t off = 0; off < n; off += batch) {
         const uint64_t cnt = n - off < batch ? n - off : batch;
         BinParams bp;
+        memset(&bp, 0, sizeof bp);
         bp.f = make_params(f, keys + off, cnt, nullptr);
         bp.recs = f->recs;
         bp.cursor = f->cursor;
@@ -504,6 +561,7 @@ int bf_get_add_mode(const bf_filter* f, int* mode, int* last_binned)
 int bf_add(bf_filter* f, const uint64_t* keys, uint64_t n, void* stream)
 {
     if (!f) return fail(BF_EINVAL, "null filter");
+    if (f->nparts > 1) return fail(BF_EINVAL, "partitioned filter: route keys with bf_route, then bf_add_routed");
     if (n == 0) return BF_OK;
     if (!keys || ((uintptr_t)keys & 7)) return fail(BF_EINVAL, "keys must be a non-null 8-byte-aligned device pointer");
     DeviceGuard g(f->device);
@@ -522,11 +580,130 @@ int bf_add(bf_filter* f, const uint64_t* keys, uint64_t n, void* stream)
 int bf_contains(const bf_filter* f, const uint64_t* keys, uint64_t n, uint32_t* out_bits, void* stream)
 {
     if (!f) return fail(BF_EINVAL, "null filter");
+    if (f->nparts > 1) return fail(BF_EINVAL, "partitioned filter: route keys with bf_route, then bf_contains_routed");
     if (n == 0) return BF_OK;
     if (!keys || ((uintptr_t)keys & 7)) return fail(BF_EINVAL, "keys must be a non-null 8-byte-aligned device pointer");
     if (!out_bits || ((uintptr_t)out_bits & 3)) return fail(BF_EINVAL, "out_bits must be a non-null 4-byte-aligned device pointer");
     DeviceGuard g(f->device);
     return launch_bulk(f, 1, keys, n, out_bits, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------ routing (NEXT N1)
+static bool routed_kernels(const bf_filter* f, KernelFn* bin, KernelFn* apply, KernelFn* test)
+{
+    if (f->variant == BF_CBF || !binned_available(f, bin, apply)) return false;
+    InstKey kt{4, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z, 1,
+               (uint8_t)f->s, 1, 0};
+    *test = registry_find(kt);
+    return *test != nullptr;
+}
+
+static BinParams routed_params(const bf_filter* f, const uint64_t* recs, const unsigned long long* counts,
+                               uint32_t nsrc, uint64_t cap)
+{
+    BinParams bp;
+    memset(&bp, 0, sizeof bp);
+    bp.f = make_params(f, nullptr, 0, nullptr);
+    bp.recs = (uint64_t*)recs;
+    bp.cursor = (unsigned long long*)counts;
+    bp.cap = cap;
+    bp.nranges = nsrc;
+    bp.blk_base = (uint32_t)f->blk_lo;
+    return bp;
+}
+
+int bf_route(const bf_filter* f, const uint64_t* keys, uint64_t n, uint64_t idx_base, uint64_t* recs, uint64_t* idx,
+             uint64_t cap, unsigned long long* counts, void* stream)
+{
+    if (!f || (n && !keys) || !recs || !counts || cap == 0 || (cap & 127) || ((uintptr_t)keys & 7))
+        return fail(BF_EINVAL, "bf_route: bad arguments (cap must be a positive multiple of 128)");
+    KernelFn bin_fn, apply_fn, test_fn;
+    if (!routed_kernels(f, &bin_fn, &apply_fn, &test_fn))
+        return fail(BF_EUNSUPPORTED, "routing kernels are not compiled for this configuration");
+    DeviceGuard g(f->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint32_t P = f->nparts;
+    cudaError_t e = cudaMemsetAsync(counts, 0, P * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return cuda_fail(e, "bf_route: counts reset");
+    if (n == 0) return BF_OK;
+    BinParams bp = routed_params(f, recs, counts, P, cap);
+    bp.f = make_params(f, keys, n, nullptr);
+    bp.f.b = f->b_global;
+    bp.f.b32 = (uint32_t)f->b_global;
+    bp.bounds = f->bounds;
+    bp.idx_out = idx;
+    bp.idx_base = idx_base;
+    static uint32_t* zero_bounds[64] = {nullptr};  // P == 1: every block is owned by part 0
+    if (!bp.bounds) {
+        int dev = f->device;
+        if (!zero_bounds[dev]) {
+            if ((e = cudaMalloc(&zero_bounds[dev], 2 * sizeof(uint32_t))) != cudaSuccess) return cuda_fail(e, "bounds");
+            cudaMemset(zero_bounds[dev], 0, 2 * sizeof(uint32_t));
+        }
+        bp.bounds = zero_bounds[dev];
+    }
+    const size_t smem = bin_smem_bytes(P);
+    cudaFuncSetAttribute((const void*)bin_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)bin_fn, BIN_THREADS, smem) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    const uint64_t chunks = (n + BIN_CHUNK - 1) / BIN_CHUNK;
+    const uint64_t grid = chunks < (uint64_t)per_sm * sm_count(f->device) ? chunks : (uint64_t)per_sm * sm_count(f->device);
+    void* args[] = {&bp};
+    if ((e = cudaLaunchKernel((const void*)bin_fn, dim3((unsigned)grid), dim3(BIN_THREADS), args, smem, st)) != cudaSuccess)
+        return cuda_fail(e, "route launch");
+    return check_launch("route launch");
+}
+
+int bf_add_routed(bf_filter* f, const uint64_t* recs, const unsigned long long* counts, uint32_t nsrc, uint64_t cap,
+                  void* stream)
+{
+    if (!f || !recs || !counts || nsrc < 1 || cap == 0 || (cap & 127)) return fail(BF_EINVAL, "bf_add_routed: bad arguments");
+    KernelFn bin_fn, apply_fn, test_fn;
+    if (!routed_kernels(f, &bin_fn, &apply_fn, &test_fn))
+        return fail(BF_EUNSUPPORTED, "routing kernels are not compiled for this configuration");
+    DeviceGuard g(f->device);
+    BinParams bp = routed_params(f, recs, counts, nsrc, cap);
+    const uint64_t tiles = (cap + 32 * f->sched[0].kpt - 1) / (32 * f->sched[0].kpt);
+    uint64_t ga = (tiles + 7) / 8;
+    const int grid_apply = pick_grid(f, apply_fn);
+    if (ga > (uint64_t)grid_apply) ga = grid_apply;
+    for (uint32_t r = 0; r < nsrc; ++r) {
+        bp.range = r;
+        void* args[] = {&bp};
+        cudaError_t e = cudaLaunchKernel((const void*)apply_fn, dim3((unsigned)ga), dim3(256), args, 0, (cudaStream_t)stream);
+        if (e != cudaSuccess) return cuda_fail(e, "apply launch");
+        if (int rc = check_launch("apply launch")) return rc;
+    }
+    return BF_OK;
+}
+
+int bf_contains_routed(const bf_filter* f, const uint64_t* recs, const unsigned long long* counts, uint32_t nsrc,
+                       uint64_t cap, uint8_t* res, void* stream)
+{
+    if (!f || !recs || !counts || !res || nsrc < 1 || cap == 0 || (cap & 127))
+        return fail(BF_EINVAL, "bf_contains_routed: bad arguments");
+    KernelFn bin_fn, apply_fn, test_fn;
+    if (!routed_kernels(f, &bin_fn, &apply_fn, &test_fn))
+        return fail(BF_EUNSUPPORTED, "routing kernels are not compiled for this configuration");
+    DeviceGuard g(f->device);
+    BinParams bp = routed_params(f, recs, counts, nsrc, cap);
+    void* args[] = {&bp, &res};
+    const int grid = pick_grid((bf_filter*)f, test_fn);
+    cudaError_t e = cudaLaunchKernel((const void*)test_fn, dim3(grid), dim3(256), args, 0, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "routed contains launch");
+    return check_launch("routed contains launch");
+}
+
+int bf_scatter_results(const uint64_t* idx, const uint8_t* res, const unsigned long long* counts, uint32_t nsrc,
+                       uint64_t cap, uint32_t* out_bits, void* stream)
+{
+    if (!idx || !res || !counts || !out_bits || nsrc < 1 || cap == 0) return fail(BF_EINVAL, "bf_scatter_results: bad arguments");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    launch_scatter_results(idx, res, counts, nsrc, cap, out_bits, (cudaStream_t)stream, 4 * sm_count(dev));
+    return check_launch("scatter launch");
 }
 
 int bf_clear(bf_filter* f, void* stream)

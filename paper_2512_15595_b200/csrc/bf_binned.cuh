@@ -37,16 +37,33 @@ struct BinParams {
     uint32_t lg_bpr;             // log2(blocks per range)
     uint32_t nranges;
     uint32_t range;              // phase 2: the range this launch applies
+    // block-range partitioned filters (NEXT N1): bin by OWNER instead of range
+    const uint32_t* bounds;      // owner p holds blocks [bounds[p], bounds[p+1]); null: range = blk >> lg_bpr
+    uint64_t* idx_out;           // optional: key index of every record (contains routing)
+    uint64_t idx_base;           // index of keys[0]
+    uint32_t blk_base;           // phase 2: first block of the local filter part
 };
 
 constexpr int BIN_THREADS = 256;
 constexpr int BIN_KPT = 8;
 constexpr int BIN_CHUNK = BIN_THREADS * BIN_KPT;  // keys per CTA chunk
 
-// dynamic smem layout: stage[CHUNK] u64 | hist[R] u32 (+pad) | gbase[R] u64 | stage_r[CHUNK] u16
+// dynamic smem layout: stage[CHUNK] u64 | hist[R] u32 (+pad) | gbase[R] u64 | stage_r[CHUNK] u16 | stage_li[CHUNK] u16
 __host__ __device__ inline size_t bin_smem_bytes(uint32_t nranges)
 {
-    return (size_t)BIN_CHUNK * 8 + (size_t)(nranges + 1) * 4 + (size_t)nranges * 8 + (size_t)BIN_CHUNK * 2;
+    return (size_t)BIN_CHUNK * 8 + (size_t)(nranges + 1) * 4 + (size_t)nranges * 8 + (size_t)BIN_CHUNK * 4;
+}
+
+// owner of a block under the partition bounds (bounds[0] = 0, bounds[P] = b)
+__device__ __forceinline__ uint32_t owner_of(const uint32_t* bounds, uint32_t P, uint32_t blk)
+{
+    uint32_t lo = 0, hi = P;  // invariant: bounds[lo] <= blk < bounds[hi]
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(bounds + mid) <= blk) lo = mid;
+        else hi = mid;
+    }
+    return lo;
 }
 
 // exclusive scan of a[0..n) in shared memory (n <= 256*32), returns the total
@@ -99,6 +116,7 @@ __global__ void __launch_bounds__(BIN_THREADS) bin_kernel(const BinParams bp)
     uint32_t* hist = (uint32_t*)(stage + BIN_CHUNK);
     unsigned long long* gbase = (unsigned long long*)(hist + R + (R & 1));
     uint16_t* stage_r = (uint16_t*)(gbase + R);
+    uint16_t* stage_li = stage_r + BIN_CHUNK;
     __shared__ uint32_t warp_tot[BIN_THREADS / 32 + 1];
 
     using W = typename C1::W;
@@ -122,7 +140,7 @@ __global__ void __launch_bounds__(BIN_THREADS) bin_kernel(const BinParams bp)
             if (li < cnt) {
                 const uint64_t h = xxh64_u64(ld_key1(p.keys + base + li), p.seed);
                 const uint32_t blk = block_of(h, p.b32);
-                const uint32_t r = blk >> bp.lg_bpr;
+                const uint32_t r = bp.bounds ? owner_of(bp.bounds, R, blk) : blk >> bp.lg_bpr;
                 rec[i] = ((uint64_t)blk << 32) | (uint32_t)h;
                 rl[i] = (r << 16) | atomicAdd(&hist[r], 1u);
             }
@@ -139,6 +157,7 @@ __global__ void __launch_bounds__(BIN_THREADS) bin_kernel(const BinParams bp)
                 const uint32_t r = rl[i] >> 16, pos = hist[r] + (rl[i] & 0xFFFFu);
                 stage[pos] = rec[i];
                 stage_r[pos] = (uint16_t)r;
+                stage_li[pos] = (uint16_t)(i * BIN_THREADS + tid);
             }
         }
         __syncthreads();
@@ -149,9 +168,10 @@ __global__ void __launch_bounds__(BIN_THREADS) bin_kernel(const BinParams bp)
             const uint64_t v = stage[j];
             if (off < bp.cap) {
                 bp.recs[(uint64_t)r * bp.cap + off] = v;
-            } else {  // bucket full: OR this key in directly (order-free)
+                if (bp.idx_out) bp.idx_out[(uint64_t)r * bp.cap + off] = bp.idx_base + base + stage_li[j];
+            } else if (!bp.bounds) {  // bucket full: OR this key in directly (order-free)
                 add_part<C1>((W*)p.words, (uint32_t)v, (uint32_t)(v >> 32), 0, ss);
-            }
+            }  // routing: dropped; the receiver sees count > cap and the host reports it
         }
         __syncthreads();
     }
@@ -202,7 +222,7 @@ __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
         if constexpr (C::THETA == 1) {
 #pragma unroll
             for (int j = 0; j < KPT; ++j)
-                if (valid[j]) add_part<C>(F, (uint32_t)rec[j], (uint32_t)(rec[j] >> 32), 0, ss);
+                if (valid[j]) add_part<C>(F, (uint32_t)rec[j], (uint32_t)(rec[j] >> 32) - bp.blk_base, 0, ss);
         } else {
 #pragma unroll 1
             for (int rr = 0; rr < C::THETA; ++rr) {
@@ -210,12 +230,36 @@ __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
 #pragma unroll
                 for (int j = 0; j < KPT; ++j) {
                     const uint32_t l = __shfl_sync(0xffffffffu, (uint32_t)rec[j], src);
-                    const uint32_t bk = __shfl_sync(0xffffffffu, (uint32_t)(rec[j] >> 32), src);
+                    const uint32_t bk = __shfl_sync(0xffffffffu, (uint32_t)(rec[j] >> 32) - bp.blk_base, src);
                     const bool v = __shfl_sync(0xffffffffu, (int)valid[j], src);
                     if (v) add_part<C>(F, l, bk, pos, ss);
                 }
             }
         }
+    }
+}
+
+// Routed lookup (NEXT N1): test the records of every source bucket against
+// the local part of the filter; one result byte per record slot.  C is a
+// Θ=1 contains configuration.
+template <class C>
+__global__ void __launch_bounds__(256) contains_bucket_kernel(const BinParams bp, uint8_t* res)
+{
+    using W = typename C::W;
+    SaltSrc<C> ss;
+    ss.init(0, nullptr, nullptr);
+    const W* F = (const W*)bp.f.words;
+    const uint64_t per = (bp.cap + 255) / 256 * 256;  // slots scanned per bucket
+    const uint64_t total = per * bp.nranges;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += stride) {
+        const uint64_t r = g / per, j = g - r * per;
+        const uint64_t cnt = min((uint64_t)bp.cursor[r], bp.cap);
+        if (j >= cnt) continue;
+        const uint64_t v = bp.recs[r * bp.cap + j];
+        W wd[C::s];
+        load_block<C>(F, (uint32_t)(v >> 32) - bp.blk_base, wd);
+        res[r * bp.cap + j] = (uint8_t)test_block<C>(wd, (uint32_t)v, ss);
     }
 }
 

@@ -11,15 +11,15 @@ typedef void (*KernelFn)(Params);
 
 // Key of a specialized kernel instantiation.
 struct InstKey {
-    uint8_t op;       // 0 add, 1 contains
+    uint8_t op;       // 0 add, 1 contains, 2 bin, 3 apply bucket, 4 contains bucket
     uint8_t variant;  // BF_BBF..BF_CSBF
     uint16_t B;
     uint8_t S, k, z, theta, phi, kpt, hv;
     uint64_t pack() const
     {
-        return (uint64_t)op | ((uint64_t)variant << 2) | ((uint64_t)(B / 32) << 5) | ((uint64_t)(S == 64) << 11) |
-               ((uint64_t)k << 12) | ((uint64_t)z << 18) | ((uint64_t)theta << 24) | ((uint64_t)phi << 30) |
-               ((uint64_t)kpt << 36) | ((uint64_t)hv << 40);
+        return (uint64_t)op | ((uint64_t)variant << 3) | ((uint64_t)(B / 32) << 6) | ((uint64_t)(S == 64) << 12) |
+               ((uint64_t)k << 13) | ((uint64_t)z << 19) | ((uint64_t)theta << 25) | ((uint64_t)phi << 31) |
+               ((uint64_t)kpt << 37) | ((uint64_t)hv << 41);
     }
 };
 
@@ -39,6 +39,9 @@ void launch_probe_red(void* buf, uint64_t b, uint32_t B, uint32_t lanes, const u
 
 void launch_probe_rng(const void* buf, uint64_t b, uint32_t B, int red, uint32_t lanes, uint64_t n,
                       cudaStream_t st, int grid);
+
+void launch_scatter_results(const uint64_t* idx, const uint8_t* res, const unsigned long long* counts,
+                            uint32_t nsrc, uint64_t cap, uint32_t* out_bits, cudaStream_t st, int grid);
 
 struct Registrar {
     Registrar(void (*fn)()) { fn(); }

@@ -280,6 +280,29 @@ void launch_probe_rng(const void* buf, uint64_t b, uint32_t B, int red, uint32_t
     }
 }
 
+// Routed lookup, last step: set bit idx of the caller's result bitmap for
+// every positive record (the bitmap is zeroed by the caller).
+__global__ void __launch_bounds__(256) scatter_results_kernel(const uint64_t* idx, const uint8_t* res,
+                                                              const unsigned long long* counts, uint32_t nsrc,
+                                                              uint64_t cap, uint32_t* out)
+{
+    const uint64_t total = cap * nsrc;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += stride) {
+        const uint64_t r = g / cap, j = g - r * cap;
+        if (j < min((uint64_t)counts[r], cap) && res[g]) {
+            const uint64_t i = idx[g];
+            atomicOr(out + (i >> 5), 1u << (i & 31));
+        }
+    }
+}
+
+void launch_scatter_results(const uint64_t* idx, const uint8_t* res, const unsigned long long* counts,
+                            uint32_t nsrc, uint64_t cap, uint32_t* out_bits, cudaStream_t st, int grid)
+{
+    scatter_results_kernel<<<grid, 256, 0, st>>>(idx, res, counts, nsrc, cap, out_bits);
+}
+
 int launch_probe_read(const void* buf, uint64_t b, uint32_t B, const uint64_t* keys, uint64_t n, uint32_t* out,
                       cudaStream_t st, int grid)
 {

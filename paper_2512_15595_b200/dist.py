@@ -90,3 +90,104 @@ def lookup_sharded(filt, keys: torch.Tensor, out: torch.Tensor | None = None) ->
     """Data-parallel lookup of this rank's shard against its replica (no
     communication)."""
     return filt.contains(keys, out)
+
+
+# --------------------------------------------------------------------------
+# Block-range partitioned filters (NEXT N1): filters larger than one GPU.
+# Owner p of P ranks holds global blocks [floor(p*b/P), floor((p+1)*b/P)).
+# add:      route (hash once, bin by owner) -> fixed-count all_to_all of the
+#           record buckets (+ their counts) -> each owner ORs what it received.
+# contains: route -> all_to_all -> owners test -> all_to_all of the result
+#           bytes back -> each sender scatters the bits to its keys' indices.
+
+class GpuRouteOps:
+    """The CUDA kernels behind the C ABI (bf_route, bf_add_routed,
+    bf_contains_routed, bf_scatter_results)."""
+
+    def __init__(self, handle):
+        from . import bf
+        self.bf, self.h = bf, handle
+
+    def route(self, keys, cap, P, want_idx):
+        dev = keys.device
+        recs = torch.empty(P * cap, dtype=torch.int64, device=dev)
+        idx = torch.empty(P * cap, dtype=torch.int64, device=dev) if want_idx else None
+        counts = torch.empty(P, dtype=torch.int64, device=dev)
+        self.bf.bf_route(self.h, keys, keys.numel(), 0, recs, idx, cap, counts)
+        return recs, idx, counts
+
+    def add_routed(self, recv, rcounts, P, cap):
+        self.bf.bf_add_routed(self.h, recv, rcounts, P, cap)
+
+    def contains_routed(self, recv, rcounts, P, cap):
+        res = torch.empty(P * cap, dtype=torch.uint8, device=recv.device)
+        self.bf.bf_contains_routed(self.h, recv, rcounts, P, cap, res)
+        return res
+
+    def scatter(self, idx, res, counts, P, cap, n):
+        out = torch.zeros((n + 31) // 32, dtype=torch.int32, device=idx.device)
+        self.bf.bf_scatter_results(idx, res, counts, P, cap, out)
+        return out
+
+
+class PartitionedFilter:
+    """One rank's part of a block-range partitioned filter."""
+
+    def __init__(self, m_bits: int, k: int, block_bits: int = 256, word_bits: int = 64, variant: int = 3,
+                 z: int = 0, seed: int = 0, group=None, ops=None, slack: float = 0.05):
+        from . import bf
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.slack = slack
+        if ops is None:
+            v = variant | (z << 8) if variant == bf.BF_CSBF else variant
+            self.handle = bf.bf_create_part(m_bits, k, block_bits, word_bits, v, seed, self.P, self.rank)
+            self.info = bf.bf_part_info(self.handle)
+            ops = GpuRouteOps(self.handle)
+        self.ops = ops
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            from . import bf
+            bf.bf_destroy(h)
+            self.handle = None
+
+    def _cap(self, n: int) -> int:
+        """Records per (sender, owner) bucket: the same on every rank (the
+        all_to_all is fixed-count), a multiple of 128."""
+        t = torch.tensor([n], dtype=torch.int64, device=self._dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        nmax = int(t.item())
+        cap = int(nmax / self.P * (1 + self.slack)) + 4096
+        return (cap + 127) // 128 * 128
+
+    def _exchange(self, send, P, cap):
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send, group=self.group)
+        return recv
+
+    def _check(self, counts, cap):
+        if int(counts.max().item()) > cap:
+            raise RuntimeError("routing bucket overflow; raise `slack`")
+
+    def add(self, keys: torch.Tensor) -> None:
+        self._dev = keys.device
+        P, cap = self.P, self._cap(keys.numel())
+        recs, _, counts = self.ops.route(keys, cap, P, False)
+        self._check(counts, cap)
+        recv = self._exchange(recs, P, cap)
+        rcounts = self._exchange(counts, P, 1)
+        self.ops.add_routed(recv, rcounts, P, cap)
+
+    def contains(self, keys: torch.Tensor) -> torch.Tensor:
+        self._dev = keys.device
+        P, cap = self.P, self._cap(keys.numel())
+        recs, idx, counts = self.ops.route(keys, cap, P, True)
+        self._check(counts, cap)
+        recv = self._exchange(recs, P, cap)
+        rcounts = self._exchange(counts, P, 1)
+        res = self.ops.contains_routed(recv, rcounts, P, cap)
+        back = self._exchange(res, P, cap)  # result bytes return to the senders' slots
+        return self.ops.scatter(idx, back, counts, P, cap, keys.numel())

@@ -465,3 +465,47 @@ def test_cbf_matches_oracle(bflib, cuda, m, k):
     want = o.bytes()
     assert np.array_equal(got[:want.size], want) and not got[want.size:].any()
     assert np.array_equal(_gpu_contains(torch, f, _to_dev(torch, q, cuda)), o.contains(q, threads=4))
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+@pytest.mark.parametrize("cfg", [(3, 256, 64, 8, 0), (4, 256, 32, 8, 2), (1, 256, 64, 8, 0), (2, 64, 64, 6, 0)])
+def test_partitioned_filter_single_gpu(bflib, cuda, cfg, P):
+    """NEXT N1 kernels on one GPU with P virtual owners: bf_route bins the keys
+    by owner, each part applies its bucket (bf_add_routed); the concatenated
+    parts equal the oracle's filter, and routed lookups (bf_contains_routed +
+    bf_scatter_results) equal the oracle's answers."""
+    import torch
+    bf = bflib
+    v, B, S, k, z = cfg
+    m = B * 40_009
+    vz = bf.BF_CSBF_Z(z) if v == 4 else v
+    parts = [bf.bf_create_part(m, k, B, S, vz, 0, P, p) for p in range(P)]
+    try:
+        keys = synth.keys(17, 120_001)
+        o = OracleFilter(v, m, B=B, S=S, k=k, z=z)
+        o.add(keys)
+        kd = _to_dev(torch, keys, cuda)
+        cap = ((120_001 // P) * 11 // 10 + 4096 + 127) // 128 * 128
+        recs = torch.empty(P * cap, dtype=torch.int64, device=cuda)
+        counts = torch.empty(P, dtype=torch.int64, device=cuda)
+        bf.bf_route(parts[0], kd, kd.numel(), 0, recs, None, cap, counts)
+        for p in range(P):
+            bf.bf_add_routed(parts[p], recs[p * cap:], counts[p:], 1, cap)
+        torch.cuda.synchronize()
+        assert int(counts.sum()) == keys.size and int(counts.max()) <= cap
+        got = np.concatenate([bf._device_view(*bf.bf_data(h)).cpu().numpy() for h in parts])
+        assert np.array_equal(got, o.bytes())
+        q = np.concatenate([keys[:30_000], synth.negatives(40_003)])
+        qd = _to_dev(torch, q, cuda)
+        idx = torch.empty(P * cap, dtype=torch.int64, device=cuda)
+        bf.bf_route(parts[0], qd, qd.numel(), 0, recs, idx, cap, counts)
+        res = torch.empty(P * cap, dtype=torch.uint8, device=cuda)
+        for p in range(P):
+            bf.bf_contains_routed(parts[p], recs[p * cap:], counts[p:], 1, cap, res[p * cap:])
+        out = torch.zeros((q.size + 31) // 32, dtype=torch.int32, device=cuda)
+        bf.bf_scatter_results(idx, res, counts, P, cap, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), o.contains(q))
+    finally:
+        for h in parts:
+            bf.bf_destroy(h)
