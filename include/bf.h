@@ -226,7 +226,9 @@ int bf_probe_red(void* buf, uint64_t b, uint32_t block_bits, uint32_t lanes,
  * the memory system's random 32-byte-sector rate alone (the paper's GUPS
  * speed of light).  red = 0: n block loads (widest loads,
  * 4 in flight per thread); red = 1: n keys, each `lanes` lanes issuing one
- * 64-bit red.global.or into their words of one random block.  The buffer's
+ * 64-bit red.global.or into their words of one random block; red = 2: n
+ * blocks OR-ed by the TMA engine (cp.reduce.async.bulk .or.b64 of the whole
+ * block from shared memory, one issuing lane per key; NEXT N4).  The buffer's
  * content is read or OR-ed; results are discarded.  n is rounded up to whole
  * iterations of the grid. */
 int bf_probe_rng(void* buf, uint64_t b, uint32_t block_bits, int red, uint32_t lanes, uint64_t n,

@@ -840,7 +840,7 @@ int bf_probe_rng(void* buf, uint64_t b, uint32_t block_bits, int red, uint32_t l
 {
     if (n == 0) return BF_OK;
     if (!buf || b < 1 || b > (1ULL << 32) || block_bits < 64 || block_bits > 1024 || !is_pow2(block_bits) ||
-        (red && (!is_pow2(lanes) || lanes > block_bits / 64)))
+        red < 0 || red > 3 || (red == 1 && (!is_pow2(lanes) || lanes > block_bits / 64)))
         return fail(BF_EINVAL, "bf_probe_rng: bad arguments");
     int dev = 0;
     cudaGetDevice(&dev);

@@ -258,10 +258,51 @@ __global__ void __launch_bounds__(256) probe_red_rng_kernel(unsigned long long* 
     }
 }
 
+// NEXT N4 experiment: the block OR issued by the TMA engine instead of the
+// LSU -- cp.reduce.async.bulk .or.b64 of one B/8-byte block from shared
+// memory per key (one issuing lane per key, every lane of the warp issues).
+__global__ void __launch_bounds__(256) probe_bulkred_rng_kernel(unsigned long long* buf, uint64_t b, uint32_t bytes,
+                                                                uint64_t iters, int hybrid)
+{
+    __shared__ __align__(128) unsigned long long src[256 * 16];  // 128 B per thread
+    for (uint32_t i = threadIdx.x; i < 256 * 16; i += blockDim.x) src[i] = 1ULL << (i & 63);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t x = mix64(tid + 0x7654321ULL) | 1ULL;
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(&src[(threadIdx.x & 255) * 16]);
+    if (hybrid && ((threadIdx.x >> 5) & 1)) {  // odd warps: the LSU path (4-lane groups, RED.64 per word)
+        const uint32_t lane = threadIdx.x & 31, pos = lane & 3, nw = bytes / 8;
+        uint64_t y = mix64(((tid >> 2) << 2) + 0x7654321ULL) | 1ULL;
+        for (uint64_t it = 0; it < iters; ++it) {
+            y = xs64(y);
+            const uint64_t blk = ((y >> 32) * b) >> 32;
+            for (uint32_t w = pos; w < nw; w += 4) red_or(buf + blk * nw + w, 1ULL << ((y >> (6 * (w & 7))) & 63));
+        }
+        return;
+    }
+    for (uint64_t it = 0; it < iters; ++it) {
+        x = xs64(x);
+        const uint64_t blk = ((x >> 32) * b) >> 32;
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.or.b64 [%0], [%1], %2;" ::"l"(
+                         buf + blk * (bytes / 8)),
+                     "r"(s), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if ((it & 7) == 7) asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 void launch_probe_rng(const void* buf, uint64_t b, uint32_t B, int red, uint32_t lanes, uint64_t n,
                       cudaStream_t st, int grid)
 {
     const uint64_t threads = (uint64_t)grid * 256;
+    if (red == 2 || red == 3) {  // 3: half the warps TMA bulk-OR, half LSU red (4 lanes per key)
+        const uint64_t iters = (n + threads - 1) / threads;
+        probe_bulkred_rng_kernel<<<grid, 256, 0, st>>>((unsigned long long*)buf, b, B / 8, iters, red == 3);
+        return;
+    }
     if (red) {
         const uint64_t groups = threads / lanes;
         const uint64_t iters = (n + groups - 1) / groups;
