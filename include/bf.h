@@ -47,6 +47,14 @@ extern "C" {
  *           `variant`: BF_CSBF_Z(z). */
 enum { BF_CBF = 0, BF_BBF = 1, BF_RBBF = 2, BF_SBF = 3, BF_CSBF = 4 };
 #define BF_CSBF_Z(z) (BF_CSBF | ((uint32_t)(z) << 8))
+/* Draw scheme in bits 16..17 of `variant` (NEXT N3 ablation):
+ *   0 multiplicative (default): d_j = lo * SALT[j] mod 2^32
+ *   1 double hashing:  d_j = lo + j * (lo(XXH64(key, seed ^ 0x9E3779B97F4A7C15)) | 1)
+ *   2 iterative:       d_j = lo(h_j), h_0 = h, h_j = XXH64(key, h_{j-1} + j)
+ * Schemes 1/2 change the bit pattern (the oracle implements them too), are
+ * compiled for SBF 256/64 (k = 8, 16), BBF 256/64 and RBBF 64/64 (k = 8)
+ * only, use the direct add path, and scheme 2 runs with Θ = 1. */
+#define BF_SCHEME(x) ((uint32_t)(x) << 16)
 
 enum {
     BF_OK = 0,

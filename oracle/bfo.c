@@ -220,6 +220,13 @@ bfo_filter* bfo_create_geometry(int variant, uint64_t m_bits, uint32_t B,
     return make(variant, m_bits, B, S, k, z, seed, 0);
 }
 
+int bfo_set_scheme(bfo_filter* f, int scheme)
+{
+    if (!f || scheme < BFO_SCHEME_MUL || scheme > BFO_SCHEME_ITER) return BFO_EINVAL;
+    f->scheme = scheme;
+    return BFO_OK;
+}
+
 void bfo_destroy(bfo_filter* f)
 {
     if (!f) return;
@@ -263,7 +270,18 @@ void bfo_pattern(const bfo_filter* f, uint64_t key, uint64_t* block, uint64_t* p
     *block = (hi * f->b) >> 32;
 
     uint32_t d[32];
-    for (uint32_t j = 0; j < f->k; ++j) d[j] = (uint32_t)(lo * SALT[j]);
+    if (f->scheme == BFO_SCHEME_DOUBLE) {
+        uint32_t lo2 = (uint32_t)key_hash(key, f->seed ^ 0x9E3779B97F4A7C15ULL) | 1u;
+        for (uint32_t j = 0; j < f->k; ++j) d[j] = lo + j * lo2;
+    } else if (f->scheme == BFO_SCHEME_ITER) {
+        uint64_t hj = h;
+        for (uint32_t j = 0; j < f->k; ++j) {
+            if (j > 0) hj = key_hash(key, hj + j);
+            d[j] = (uint32_t)hj;
+        }
+    } else {
+        for (uint32_t j = 0; j < f->k; ++j) d[j] = (uint32_t)(lo * SALT[j]);
+    }
 
     uint32_t lgS = log2u(f->S);
     if (f->variant == BFO_BBF || f->variant == BFO_RBBF) {

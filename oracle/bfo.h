@@ -43,7 +43,19 @@ typedef struct bfo_filter {
     uint64_t nbits;      /* m_eff = b*B   (CBF: m)                                  */
     uint64_t nbytes;     /* storage bytes = ceil(nbits/8)                           */
     uint8_t* bits;       /* the bit array                                           */
+    int      scheme;     /* draw scheme (bfo_set_scheme): 0 multiplicative (default) */
 } bfo_filter;
+
+/* Draw schemes of P:L223-225 (N3):
+ *   0 multiplicative: d_j = lo * SALT[j] mod 2^32                  (default)
+ *   1 double hashing: g = XXH64(le64(key), seed ^ 0x9E3779B97F4A7C15),
+ *                     d_j = lo + j * (lo(g) | 1) mod 2^32          ("Double hashing")
+ *   2 iterative:      h_0 = h, h_j = XXH64(le64(key), h_{j-1} + j), d_j = lo(h_j)
+ *                                                                  ("a single hash function iteratively")
+ * The block index always comes from h; the CSBF group selector always uses
+ * lo * GSALT[i].  CBF ignores the scheme. */
+enum { BFO_SCHEME_MUL = 0, BFO_SCHEME_DOUBLE = 1, BFO_SCHEME_ITER = 2 };
+int bfo_set_scheme(bfo_filter* f, int scheme);
 
 /* XXH64 of an arbitrary byte string (xxHash spec; "64-bit implementation
  * of the xxHash algorithm").  The filter hashes the 8 little-endian bytes of

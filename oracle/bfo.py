@@ -61,6 +61,8 @@ def lib():
             L.bfo_contains.argtypes = [vp, vp, u64, vp, i32]
             L.bfo_add_range.restype = i32
             L.bfo_add_range.argtypes = [vp, vp, u64, u64, u64, vp, i32]
+            L.bfo_set_scheme.restype = i32
+            L.bfo_set_scheme.argtypes = [vp, i32]
             L.bfo_popcount.restype = u64
             L.bfo_popcount.argtypes = [vp]
             _lib = L
@@ -71,7 +73,7 @@ class _Geom(C.Structure):
     _fields_ = [("variant", C.c_int), ("m_bits", C.c_uint64), ("B", C.c_uint32),
                 ("S", C.c_uint32), ("k", C.c_uint32), ("z", C.c_uint32),
                 ("seed", C.c_uint64), ("b", C.c_uint64), ("s", C.c_uint32),
-                ("nbits", C.c_uint64), ("nbytes", C.c_uint64), ("bits", C.c_void_p)]
+                ("nbits", C.c_uint64), ("nbytes", C.c_uint64), ("bits", C.c_void_p), ("scheme", C.c_int)]
 
 
 def xxh64(data: bytes, seed: int = 0) -> int:
@@ -105,13 +107,16 @@ class OracleFilter:
     """A bit-array Bloom filter computed key by key (oracle/bfo.c)."""
 
     def __init__(self, variant: int, m_bits: int, B: int = 256, S: int = 64, k: int = 8,
-                 z: int = 0, seed: int = 0, allocate: bool = True):
+                 z: int = 0, seed: int = 0, allocate: bool = True, scheme: int = 0):
         L = lib()
         fn = L.bfo_create if allocate else L.bfo_create_geometry
         self._p = fn(variant, m_bits, B, S, k, z, seed)
         if not self._p:
             raise ValueError(f"invalid oracle config variant={variant} m={m_bits} B={B} "
                              f"S={S} k={k} z={z}")
+        if L.bfo_set_scheme(self._p, scheme) != 0:
+            raise ValueError(f"invalid draw scheme {scheme}")
+        self.scheme = scheme
         g = _Geom.from_address(self._p)
         self.variant, self.m_bits, self.B, self.S = variant, m_bits, g.B, g.S
         self.k, self.z, self.seed = g.k, g.z, g.seed

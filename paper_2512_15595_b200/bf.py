@@ -34,6 +34,11 @@ def BF_CSBF_Z(z: int) -> int:
     return BF_CSBF | (z << 8)
 
 
+def BF_SCHEME(x: int) -> int:
+    """Draw scheme bits of `variant`: 0 multiplicative, 1 double hashing, 2 iterative."""
+    return x << 16
+
+
 _u64, _u32, _i32, _vp = C.c_uint64, C.c_uint32, C.c_int, C.c_void_p
 _SIGS = {
     "bf_create": (_vp, [_u64, _u32, _u32, _u32, _u32]),
@@ -253,10 +258,11 @@ class Filter:
     """
 
     def __init__(self, m_bits: int, k: int, block_bits: int = 256, word_bits: int = 64,
-                 variant: str | int = "SBF", z: int = 0, seed: int = 0):
+                 variant: str | int = "SBF", z: int = 0, seed: int = 0, scheme: int = 0):
         v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
         if v == BF_CSBF and z:
             v = BF_CSBF_Z(z)
+        v |= BF_SCHEME(scheme)
         self.m_bits, self.k, self.B, self.S = m_bits, k, block_bits, word_bits
         self.variant, self.z, self.seed = v & 0xFF, z, seed
         self.handle = bf_create(m_bits, k, block_bits, word_bits, v, seed)

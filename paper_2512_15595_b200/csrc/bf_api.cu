@@ -119,6 +119,7 @@ struct Sched {
 struct bf_filter {
     int device;
     uint32_t variant, z, k, B, S, s;
+    uint32_t scheme;  // draw scheme (variant bits 16..17): 0 multiplicative, 1 double, 2 iterative
     uint64_t m_bits, b, bytes, seed;
     void* words;
     Sched sched[2];  // [0] add, [1] contains
@@ -155,7 +156,7 @@ static int validate(uint64_t m_bits, uint32_t k, uint32_t B, uint32_t S, uint32_
         return BF_OK;
     }
     if (v != BF_BBF && v != BF_RBBF && v != BF_SBF && v != BF_CSBF) return fail(BF_EINVAL, "unknown variant %u", v);
-    if (variant >> 16) return fail(BF_EINVAL, "unknown variant bits 0x%x", variant);
+    if ((variant >> 18) || ((variant >> 16) & 3) == 3) return fail(BF_EINVAL, "unknown variant bits 0x%x", variant);
     if (S != 32 && S != 64) return fail(BF_EINVAL, "word_bits must be 32 or 64 (got %u)", S);
     if (!is_pow2(B) || B < S || B > 1024) return fail(BF_EINVAL, "block_bits must be a power of two in [S, 1024] (got %u)", B);
     if (k < 1 || k > 32) return fail(BF_EINVAL, "k must be in 1..32 (got %u)", k);
@@ -190,14 +191,21 @@ static int set_sched(bf_filter* f, int op, int theta, int phi, int kpt, int hv)
         else { theta = f->B > 256 ? (int)f->B / 256 : 1; phi = s / theta; }  // Θ̂_c = max(1, B/256)
         kpt = 4;  // 4 keys per lane: one 256-bit key load, 4 blocks in flight (profiles/r1_sweep_c2.md)
         hv = 0;
+        if (f->scheme == 2) {  // iterative draws form a chain per key: one lane per key
+            theta = 1;
+            phi = s;
+            kpt = 1;
+        }
     }
     if (!is_pow2(theta) || !is_pow2(phi) || theta * phi > s || theta > 32)
         return fail(BF_EINVAL, "invalid layout Θ=%d Φ=%d for s=%d (need powers of two, Θ·Φ <= s)", theta, phi, s);
     if (kpt != 1 && kpt != 2 && kpt != 4) return fail(BF_EINVAL, "kpt must be 1, 2 or 4");
     if (hv < 0 || hv > 3) return fail(BF_EINVAL, "hash_variant must be 0..3");
     InstKey key{(uint8_t)op, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z,
-                (uint8_t)theta, (uint8_t)phi, (uint8_t)kpt, (uint8_t)hv};
+                (uint8_t)theta, (uint8_t)phi, (uint8_t)kpt, (uint8_t)hv, (uint8_t)f->scheme};
     KernelFn fn = f->variant == BF_CBF ? nullptr : registry_find(key);
+    if (!fn && f->scheme != 0)
+        return fail(BF_EUNSUPPORTED, "draw scheme %u is compiled only for selected configurations", f->scheme);
     Sched sc{theta, phi, kpt, hv, fn, fn != nullptr, 0};
     if (f->variant == BF_CBF) sc = Sched{1, 1, 1, 0, cbf_entry(op == 0, (int)f->k), false, 0};
     if (!fn && f->variant != BF_CBF) {
@@ -247,6 +255,7 @@ static bf_filter* create_impl(uint64_t m_bits, uint32_t k, uint32_t block_bits, 
         return nullptr;
     }
     f->variant = variant & 0xFF;
+    f->scheme = (variant >> 16) & 3;
     f->z = z;
     f->k = k;
     if (f->variant == BF_CBF) {  // one "block" per 32-bit word; positions span all m bits
@@ -386,7 +395,7 @@ int bf_set_layout(bf_filter* f, int op, int theta, int phi, int kpt, int hash_va
     if (kpt != 1 && kpt != 2 && kpt != 4) return fail(BF_EINVAL, "kpt must be 1, 2 or 4");
     if (hash_variant < 0 || hash_variant > 3) return fail(BF_EINVAL, "hash_variant must be 0..3");
     InstKey key{(uint8_t)op, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z,
-                (uint8_t)theta, (uint8_t)phi, (uint8_t)kpt, (uint8_t)hash_variant};
+                (uint8_t)theta, (uint8_t)phi, (uint8_t)kpt, (uint8_t)hash_variant, (uint8_t)f->scheme};
     if (!registry_find(key))
         return fail(BF_EUNSUPPORTED, "schedule Θ=%d Φ=%d kpt=%d hv=%d not compiled for this configuration", theta,
                     phi, kpt, hash_variant);
@@ -446,7 +455,7 @@ static const uint64_t kBinMinFilterBytes = 96ULL << 20;  // below this the filte
 static bool binned_available(const bf_filter* f, KernelFn* bin, KernelFn* apply)
 {
     const Sched& sc = f->sched[0];
-    if (!sc.specialized) return false;
+    if (!sc.specialized || f->scheme != 0) return false;  // records carry lo only
     InstKey kb{2, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z, 1, 1, 1, 0};
     InstKey ka{3, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z,
                (uint8_t)sc.theta, (uint8_t)sc.phi, (uint8_t)sc.kpt, (uint8_t)sc.hv};

@@ -15,11 +15,12 @@ struct InstKey {
     uint8_t variant;  // BF_BBF..BF_CSBF
     uint16_t B;
     uint8_t S, k, z, theta, phi, kpt, hv;
+    uint8_t hs = 0;   // draw scheme (0 multiplicative, 1 double hashing, 2 iterative)
     uint64_t pack() const
     {
         return (uint64_t)op | ((uint64_t)variant << 3) | ((uint64_t)(B / 32) << 6) | ((uint64_t)(S == 64) << 12) |
                ((uint64_t)k << 13) | ((uint64_t)z << 19) | ((uint64_t)theta << 25) | ((uint64_t)phi << 31) |
-               ((uint64_t)kpt << 37) | ((uint64_t)hv << 41);
+               ((uint64_t)kpt << 37) | ((uint64_t)hv << 41) | ((uint64_t)hs << 45);
     }
 };
 

@@ -47,11 +47,15 @@ struct Params {
     uint32_t variant, B, S, k, z;
 };
 
-template <int V_, int S_, int LGS_, int K_, int Z_, int THETA_, int PHI_, int KPT_, int HV_>
+template <int V_, int S_, int LGS_, int K_, int Z_, int THETA_, int PHI_, int KPT_, int HV_, int HS_ = 0>
 struct Cfg {
     static constexpr int V = V_, S = S_, s = 1 << LGS_, K = K_;
     static constexpr int Z = (V_ == V_CSBF) ? Z_ : 1;
     static constexpr int THETA = THETA_, PHI = PHI_, KPT = KPT_, HV = HV_;
+    // draw scheme (N3): 0 multiplicative, 1 double hashing, 2 iterative
+    static constexpr int HS = HS_;
+    static_assert(HS >= 0 && HS <= 2, "draw scheme");
+    static_assert(HS != 2 || THETA_ == 1, "the iterative scheme's draws form a chain: Θ = 1 only");
     static constexpr int B = S * s, LGB = ilog2(B), LGW = ilog2(S);
     static constexpr int G = (V == V_CSBF) ? s / Z : 1, LGG = ilog2(G);
     static constexpr int Q = (V == V_SBF || V == V_RBBF) ? K / s : (V == V_CSBF ? K / Z : K);
@@ -136,31 +140,77 @@ template <class C> struct SaltSrc {
     }
 };
 
+// ----------------------------------------------------------------- draws
+// The k draw values d_j of one key (DESIGN.md section 2 and the N3 schemes):
+//   HS 0 multiplicative  d_j = lo * SALT[j]            (salts: immediates / registers)
+//   HS 1 double hashing  d_j = lo + j * lo2,  lo2 = lo(XXH64(key, seed ^ phi64)) | 1
+//   HS 2 iterative       d_j = lo(h_j), h_0 = h, h_j = XXH64(key, h_{j-1} + j)
+// lo also drives the CSBF group selector in every scheme.
+constexpr uint64_t DOUBLE_HASH_SEED_XOR = 0x9E3779B97F4A7C15ULL;
+
+template <class C> struct Draws {
+    uint32_t lo;
+    uint32_t lo2;
+    uint32_t d[C::HS == 2 ? C::K : 1];
+    __device__ __forceinline__ Draws(uint32_t lo_) : lo(lo_), lo2(0) {}  // HS 0 (records, shuffles)
+    __device__ __forceinline__ Draws(uint32_t lo_, uint32_t lo2_) : lo(lo_), lo2(lo2_) {}
+    // the whole key -> draws step for one key
+    static __device__ __forceinline__ Draws make(uint64_t key, uint64_t h, uint64_t seed)
+    {
+        Draws r((uint32_t)h, 0);
+        if constexpr (C::HS == 1) r.lo2 = (uint32_t)xxh64_u64(key, seed ^ DOUBLE_HASH_SEED_XOR) | 1u;
+        if constexpr (C::HS == 2) {
+            uint64_t hj = h;
+#pragma unroll
+            for (int j = 0; j < C::K; ++j) {
+                if (j > 0) hj = xxh64_u64(key, hj + (uint64_t)j);
+                r.d[j] = (uint32_t)hj;
+            }
+        }
+        return r;
+    }
+    // draw T of slot SLOT (word w) for SBF/CSBF
+    template <int SLOT, int T>
+    __device__ __forceinline__ uint32_t word_draw(uint32_t w, const SaltSrc<C>& ss) const
+    {
+        if constexpr (C::HS == 0) return lo * ss.template salt<SLOT, T>(w);
+        else if constexpr (C::HS == 1) return lo + C::draw(w, T) * lo2;
+        else return d[C::draw((uint32_t)SLOT, T)];  // Θ == 1: word == slot, compile-time
+    }
+    // draw J of a BBF pattern
+    template <int J> __device__ __forceinline__ uint32_t bbf_draw(const SaltSrc<C>& ss) const
+    {
+        if constexpr (C::HS == 0) return lo * ss.template bbf_salt<J>();
+        else if constexpr (C::HS == 1) return lo + (uint32_t)J * lo2;
+        else return d[J];
+    }
+};
+
 // ----------------------------------------------------------------- pattern
-// Mask of word w (slot SLOT of this lane) for a key with low hash half lo,
+// Mask of word w (slot SLOT of this lane) for a key with draws dr,
 // DESIGN.md section 2 / P:L115-132.
 template <class C, int SLOT>
-__device__ __forceinline__ typename C::W slot_mask(uint32_t lo, uint32_t w, const SaltSrc<C>& ss)
+__device__ __forceinline__ typename C::W slot_mask(const Draws<C>& dr, uint32_t w, const SaltSrc<C>& ss)
 {
     using W = typename C::W;
     W m = 0;
     if constexpr (C::V == V_SBF || C::V == V_RBBF) {
         StaticFor<0, C::Q>::run([&](auto T) {
-            const uint32_t d = lo * ss.template salt<SLOT, decltype(T)::value>(w);
+            const uint32_t d = dr.template word_draw<SLOT, decltype(T)::value>(w, ss);
             m |= W(1) << (d >> (32 - C::LGW));
         });
     } else if constexpr (C::V == V_CSBF) {
         StaticFor<0, C::Q>::run([&](auto T) {
-            const uint32_t d = lo * ss.template salt<SLOT, decltype(T)::value>(w);
+            const uint32_t d = dr.template word_draw<SLOT, decltype(T)::value>(w, ss);
             m |= W(1) << (d >> (32 - C::LGW));
         });
         if constexpr (C::G > 1) {
-            const uint32_t sel = (lo * ss.template gsalt<SLOT>(w)) >> (32 - C::LGG);
+            const uint32_t sel = (dr.lo * ss.template gsalt<SLOT>(w)) >> (32 - C::LGG);
             m = ((w & (C::G - 1)) == sel) ? m : W(0);
         }
     } else {  // BBF: k draws over the whole block; keep those landing in word w
         StaticFor<0, C::K>::run([&](auto J) {
-            const uint32_t p = (lo * ss.template bbf_salt<decltype(J)::value>()) >> (32 - C::LGB);
+            const uint32_t p = dr.template bbf_draw<decltype(J)::value>(ss) >> (32 - C::LGB);
             m |= shl_clamp(W(1), p - w * (uint32_t)C::S);
         });
     }
@@ -195,7 +245,7 @@ __device__ __forceinline__ void load_block(const typename C::W* F, uint32_t blk,
 // the answer ("If any bit is zero, the element is certainly not in the
 // set").
 template <class C>
-__device__ __forceinline__ bool test_block(const typename C::W* wd, uint32_t lo, const SaltSrc<C>& ss)
+__device__ __forceinline__ bool test_block(const typename C::W* wd, const Draws<C>& dr, const SaltSrc<C>& ss)
 {
     using W = typename C::W;
     uint32_t acc = 0xffffffffu;
@@ -203,7 +253,7 @@ __device__ __forceinline__ bool test_block(const typename C::W* wd, uint32_t lo,
         StaticFor<0, C::s>::run([&](auto I) {
             constexpr int w = decltype(I)::value;
             StaticFor<0, C::Q>::run([&](auto T) {
-                const uint32_t d = lo * ss.template salt<w, decltype(T)::value>((uint32_t)w);
+                const uint32_t d = dr.template word_draw<w, decltype(T)::value>((uint32_t)w, ss);
                 acc &= (uint32_t)(wd[w] >> (d >> (32 - C::LGW)));
             });
         });
@@ -212,19 +262,19 @@ __device__ __forceinline__ bool test_block(const typename C::W* wd, uint32_t lo,
             constexpr int w0 = decltype(I)::value * C::G;  // first word of group i
             W x;
             if constexpr (C::G > 1) {
-                const uint32_t sel = (lo * ss.template gsalt<w0>((uint32_t)w0)) >> (32 - C::LGG);
+                const uint32_t sel = (dr.lo * ss.template gsalt<w0>((uint32_t)w0)) >> (32 - C::LGG);
                 x = pick<C::G>(wd + w0, sel);
             } else {
                 x = wd[w0];
             }
             StaticFor<0, C::Q>::run([&](auto T) {
-                const uint32_t d = lo * ss.template salt<w0, decltype(T)::value>((uint32_t)w0);
+                const uint32_t d = dr.template word_draw<w0, decltype(T)::value>((uint32_t)w0, ss);
                 acc &= (uint32_t)(x >> (d >> (32 - C::LGW)));
             });
         });
     } else {  // BBF
         StaticFor<0, C::K>::run([&](auto J) {
-            const uint32_t p = (lo * ss.template bbf_salt<decltype(J)::value>()) >> (32 - C::LGB);
+            const uint32_t p = dr.template bbf_draw<decltype(J)::value>(ss) >> (32 - C::LGB);
             const W x = (C::s > 1) ? pick<C::s>(wd, p >> C::LGW) : wd[0];
             acc &= (uint32_t)(x >> (p & (C::S - 1)));
         });
@@ -234,7 +284,7 @@ __device__ __forceinline__ bool test_block(const typename C::W* wd, uint32_t lo,
 
 // contains, this lane's words of a block (Θ > 1): returns the missing bits.
 template <class C>
-__device__ __forceinline__ typename C::W contains_part(const typename C::W* F, uint32_t lo, uint32_t blk,
+__device__ __forceinline__ typename C::W contains_part(const typename C::W* F, const Draws<C>& dr, uint32_t blk,
                                                       uint32_t pos, const SaltSrc<C>& ss)
 {
     using W = typename C::W;
@@ -245,7 +295,7 @@ __device__ __forceinline__ typename C::W contains_part(const typename C::W* F, u
     });
     W acc = 0;
     StaticFor<0, C::NSLOT>::run([&](auto SL) {
-        const W m = slot_mask<C, decltype(SL)::value>(lo, C::word(decltype(SL)::value, pos), ss);
+        const W m = slot_mask<C, decltype(SL)::value>(dr, C::word(decltype(SL)::value, pos), ss);
         acc |= m & ~wd[decltype(SL)::value];
     });
     return acc;
@@ -253,14 +303,14 @@ __device__ __forceinline__ typename C::W contains_part(const typename C::W* F, u
 
 // add, this lane's words of a block (pos = 0 and all words when Θ == 1).
 template <class C>
-__device__ __forceinline__ void add_part(typename C::W* F, uint32_t lo, uint32_t blk, uint32_t pos,
+__device__ __forceinline__ void add_part(typename C::W* F, const Draws<C>& dr, uint32_t blk, uint32_t pos,
                                          const SaltSrc<C>& ss)
 {
     using W = typename C::W;
     W* bp = F + (uint64_t)blk * C::s;
     StaticFor<0, C::NSLOT>::run([&](auto SL) {
         const uint32_t w = (C::THETA == 1) ? (uint32_t)decltype(SL)::value : C::word(decltype(SL)::value, pos);
-        const W m = slot_mask<C, decltype(SL)::value>(lo, w, ss);
+        const W m = slot_mask<C, decltype(SL)::value>(dr, w, ss);
         if constexpr (C::V == V_SBF || C::V == V_RBBF) {
             red_or(bp + w, m);  // every SBF word receives >= 1 bit
         } else {
@@ -349,13 +399,16 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
             key[j] = valid[j] ? ld_key1(p.keys + mine + j) : 0ULL;
         }
     }
-    uint32_t lo[KPT], blk[KPT];
+    uint32_t lo[KPT], blk[KPT], lo2[KPT];
+    uint64_t hfull[KPT];
     if constexpr (!(C::HV == 3 && C::THETA > 1)) {
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
             const uint64_t h = xxh64_u64(key[j], p.seed);
             lo[j] = (uint32_t)h;
             blk[j] = block_of(h, p.b32);
+            hfull[j] = h;
+            if constexpr (C::HS == 1) lo2[j] = Draws<C>::make(key[j], h, p.seed).lo2;
         }
     }
 
@@ -366,7 +419,7 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
     if constexpr (C::THETA == 1 && ADD) {
 #pragma unroll
         for (int j = 0; j < KPT; ++j)
-            if (FULL || valid[j]) add_part<C>((W*)p.words, lo[j], blk[j], 0, ss);
+            if (FULL || valid[j]) add_part<C>((W*)p.words, Draws<C>::make(key[j], hfull[j], p.seed), blk[j], 0, ss);
     } else if constexpr (C::THETA == 1) {
         // issue every block load of the tile before testing any (memory-level
         // parallelism: KPT*s/Φ loads in flight per lane), then the next
@@ -381,7 +434,8 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
         }
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
-            if (FULL || valid[j]) res |= (uint32_t)test_block<C>(wd[j], lo[j], ss) << j;
+            if (FULL || valid[j])
+                res |= (uint32_t)test_block<C>(wd[j], Draws<C>::make(key[j], hfull[j], p.seed), ss) << j;
         }
     } else {
         // (2) group-cooperative execution, one key of the group at a time
@@ -391,23 +445,27 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
             const uint32_t src = gbase + r;
 #pragma unroll
             for (int j = 0; j < KPT; ++j) {
-                uint32_t l, bk;
+                uint32_t l, bk, l2 = 0;
                 bool v;
                 if constexpr (C::HV == 3) {  // ablation: every lane re-hashes the key itself
                     const uint64_t idx = base + (uint64_t)src * KPT + j;
                     v = FULL || idx < p.n;
-                    const uint64_t h = xxh64_u64(v ? p.keys[idx] : 0ULL, p.seed);
+                    const uint64_t kk = v ? p.keys[idx] : 0ULL;
+                    const uint64_t h = xxh64_u64(kk, p.seed);
                     l = (uint32_t)h;
                     bk = block_of(h, p.b32);
+                    if constexpr (C::HS == 1) l2 = Draws<C>::make(kk, h, p.seed).lo2;
                 } else {
                     l = __shfl_sync(0xffffffffu, lo[j], src);
                     bk = __shfl_sync(0xffffffffu, blk[j], src);
+                    if constexpr (C::HS == 1) l2 = __shfl_sync(0xffffffffu, lo2[j], src);
                     v = FULL || __shfl_sync(0xffffffffu, (int)valid[j], src);
                 }
+                const Draws<C> dr(l, l2);
                 if constexpr (ADD) {
-                    if (v) add_part<C>((W*)p.words, l, bk, pos, ss);
+                    if (v) add_part<C>((W*)p.words, dr, bk, pos, ss);
                 } else {
-                    const W miss = v ? contains_part<C>((const W*)p.words, l, bk, pos, ss) : W(0);
+                    const W miss = v ? contains_part<C>((const W*)p.words, dr, bk, pos, ss) : W(0);
                     const uint32_t ball = __ballot_sync(0xffffffffu, miss != 0);
                     const uint32_t ok = (((ball >> gbase) & GMASK) == 0) && v;
                     if (pos == (uint32_t)r) res |= ok << j;

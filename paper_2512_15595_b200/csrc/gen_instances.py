@@ -106,10 +106,27 @@ def instances():
     return sorted(inst)
 
 
+def scheme_instances():
+    """Pattern-changing draw schemes (NEXT N3): double hashing (1) and
+    the iterative single hash (2), for the hashing ablation rows.  Tuples carry
+    an 11th field, the scheme."""
+    out = []
+    for v, B, S, k in [(SBF, 256, 64, 16), (SBF, 256, 64, 8), (BBF, 256, 64, 8), (RBBF, 64, 64, 8)]:
+        s = B // S
+        for op in (0, 1):
+            out.append((op, v, B, S, k, 0, 1, s, 1, 0, 2))      # iterative: Θ = 1 only
+            out.append((op, v, B, S, k, 0, 1, s, 4, 0, 1))      # double hashing, Θ = 1
+            if op == 0 and s > 1:
+                out.append((op, v, B, S, k, 0, s, 1, 4, 0, 1))  # double hashing, add Θ = s
+    return out
+
+
 def cfg_type(i):
-    op, v, B, S, k, z, theta, phi, kpt, hv = i
+    op, v, B, S, k, z, theta, phi, kpt, hv = i[:10]
+    hs = i[10] if len(i) > 10 else 0
     lgs = (B // S).bit_length() - 1
-    return f"Cfg<{VNAME[v]}, {S}, {lgs}, {k}, {z}, {theta}, {phi}, {kpt}, {hv}>"
+    extra = f", {hs}" if hs else ""
+    return f"Cfg<{VNAME[v]}, {S}, {lgs}, {k}, {z}, {theta}, {phi}, {kpt}, {hv}{extra}>"
 
 
 def emit():
@@ -126,14 +143,15 @@ def emit():
             binned.append((2, v, B, S, k, z, 1, 1, 1, 0))
             binned.append((3, v, B, S, k, z, theta, phi, kpt, hv))
             binned.append((4, v, B, S, k, z, 1, B // S, 1, 0))  # routed contains (Θ=1, Φ=s)
-    inst = inst + binned
+    inst = inst + binned + scheme_instances()
     shards = [inst[i::NSHARDS] for i in range(NSHARDS)]
     for si, sh in enumerate(shards):
         lines = ["// GENERATED by csrc/gen_instances.py -- do not edit.",
                  '#include "../bf_internal.h"', '#include "../bf_kernels.cuh"', '#include "../bf_binned.cuh"', "",
                  "namespace bf {", "namespace {", "void reg() {"]
         for i in sh:
-            op, v, B, S, k, z, theta, phi, kpt, hv = i
+            op, v, B, S, k, z, theta, phi, kpt, hv = i[:10]
+            hs = i[10] if len(i) > 10 else 0
             if op == 2:
                 fn = f"bin_kernel<{cfg_type(i)}>"
             elif op == 3:
@@ -142,7 +160,7 @@ def emit():
                 fn = f"contains_bucket_kernel<{cfg_type(i)}>"
             else:
                 fn = f"bulk_kernel<{cfg_type(i)}, {'true' if op == 0 else 'false'}>"
-            lines.append(f"    registry_add(InstKey{{{op}, {v}, {B}, {S}, {k}, {z}, {theta}, {phi}, {kpt}, {hv}}}, "
+            lines.append(f"    registry_add(InstKey{{{op}, {v}, {B}, {S}, {k}, {z}, {theta}, {phi}, {kpt}, {hv}, {hs}}}, "
                          f"(KernelFn){fn});")
         lines += ["}", "Registrar r_(reg);", "}  // namespace", "}  // namespace bf", ""]
         with open(os.path.join(GEN, f"inst_{si:02d}.cu"), "w") as fh:

@@ -509,3 +509,33 @@ def test_partitioned_filter_single_gpu(bflib, cuda, cfg, P):
     finally:
         for h in parts:
             bf.bf_destroy(h)
+
+
+SCHEME_CFGS = [(3, 256, 64, 16), (3, 256, 64, 8), (1, 256, 64, 8), (2, 64, 64, 8)]
+
+
+@pytest.mark.parametrize("scheme", [1, 2])
+@pytest.mark.parametrize("cfg", SCHEME_CFGS)
+def test_draw_schemes_match_oracle(bflib, cuda, cfg, scheme):
+    """NEXT N3: the double-hashing and iterative draw schemes on the
+    GPU == the oracle's, every compiled schedule (bits and answers)."""
+    import torch
+    bf = bflib
+    v, B, S, k = cfg
+    m = B * 3001
+    keys = synth.keys(23, N_ADD)
+    q = np.concatenate([keys[::3], synth.negatives(N_NEG)])
+    o = OracleFilter(v, m, B=B, S=S, k=k, scheme=scheme)
+    o.add(keys)
+    kd, qd = _to_dev(torch, keys, cuda), _to_dev(torch, q, cuda)
+    f = bf.Filter(m, k, B, S, variant=v, scheme=scheme)
+    s = B // S
+    scheds = [(0, 1, s, 1 if scheme == 2 else 4)] + ([(0, s, 1, 4)] if scheme == 1 and s > 1 else [])
+    for op, th, ph, kpt in scheds:
+        f.set_layout(op, th, ph, kpt, 0)
+        f.clear()
+        f.add(kd)
+        torch.cuda.synchronize()
+        assert np.array_equal(_gpu_bytes(f), o.bytes()), (op, th, ph, kpt)
+    f.set_layout(1, 1, s, 1 if scheme == 2 else 4, 0)
+    assert np.array_equal(_gpu_contains(torch, f, qd), o.contains(q))

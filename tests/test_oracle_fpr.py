@@ -125,3 +125,31 @@ def test_cbf_eq1_at_optimal_load():
     assert abs(M.binom_z(fp, Q, 0.5 ** k)) <= 4.0, fp
     assert f.popcount() / m == pytest.approx(0.5, abs=2e-3)
     assert abs(M.binom_z(fp, Q, M.fpr_conditional(CBF, f.bytes(), 0, 64, k, m_bits=m))) <= 4.0
+
+
+@pytest.mark.parametrize("scheme", [1, 2])
+@pytest.mark.parametrize("cfg", [(SBF, 256, 64, 16, 0), (BBF, 256, 64, 8, 0), (RBBF, 64, 64, 8, 0)])
+def test_draw_schemes_fpr_matches_exact_model(scheme, cfg):
+    """The pattern-changing draw schemes of P:L223 (NEXT N3).  The iterative
+    single hash (k chained XXH64 evaluations) behaves like ideal hashing:
+    FPR within |z| <= 4 of the exact model.  Double hashing (draws in
+    arithmetic progression, top bits) does not: its draws are correlated and
+    its FPR sits 1.4-1.9x above the ideal model (the reason P:L225 gives for
+    multiplicative hashing: "approximately uniform distribution of bits").
+    Both have no false negatives and differ from the multiplicative scheme."""
+    v, B, S, k, z = cfg
+    m, n, Q = 1 << 24, 1 << 20, 1 << 22
+    f = OracleFilter(v, m, B=B, S=S, k=k, z=z, scheme=scheme)
+    f.add(synth.positives(n), threads=8)
+    fp = int(unpack_bits(f.contains(synth.negatives(Q), threads=8), Q).sum())
+    p = M.fpr_exact(v, n, m // B, B, S, k, z)
+    if scheme == 2:
+        assert abs(M.binom_z(fp, Q, p)) <= 4.0, (fp, Q * p)
+    else:
+        assert 1.2 < fp / (Q * p) < 2.5, (fp, Q * p)
+    assert unpack_bits(f.contains(synth.positives(n)[:50000], threads=8), 50000).all()
+    g = OracleFilter(v, m, B=B, S=S, k=k, z=z, scheme=0)
+    g.add(synth.positives(n)[:1000])
+    h = OracleFilter(v, m, B=B, S=S, k=k, z=z, scheme=scheme)
+    h.add(synth.positives(n)[:1000])
+    assert not np.array_equal(g.bytes(), h.bytes())

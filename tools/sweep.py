@@ -45,7 +45,7 @@ def c_iso(variant, B, S, k, z):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--set", default="c2", choices=["c2", "c2iso", "c4", "c4l2", "one", "paper"])
+    ap.add_argument("--set", default="c2", choices=["c2", "c2iso", "c4", "c4l2", "one", "paper", "ablation"])
     ap.add_argument("--n", type=int, default=1 << 26)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cfg", default=None, help="v,B,S,k,z for --set one")
@@ -61,6 +61,8 @@ def main():
         return iso_sweep(a, torch, bf, dev)
     if a.set == "paper":
         return paper_tables(a, torch, bf, dev)
+    if a.set == "ablation":
+        return hash_ablation(a, torch, bf, dev)
     inst = instances()
     groups = defaultdict(list)
     for op, v, B, S, k, z, th, ph, kpt, hv in inst:
@@ -224,6 +226,61 @@ def paper_tables(a, torch, bf, dev):
                 print(json.dumps(rec), flush=True)
                 if fh:
                     fh.write(json.dumps(rec) + "\n")
+            del f
+
+
+def hash_ablation(a, torch, bf, dev):
+    """The paper's optimisation breakdown (Fig. 9) on SBF 256/64
+    k=16: GPU CBF -> SBF with iterative single-hash draws (one XXH64 per draw,
+    P:L223) -> double hashing -> multiplicative hashing, each at the
+    unoptimised layout (Θ=1, KPT=1) and at the optimised one (add Θ=s with
+    cooperation, KPT=4)."""
+    n = a.n
+    keys = torch.empty(n, dtype=torch.int64, device=dev)
+    bf.bf_keygen(keys, n, 0)
+    out = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fh = open(a.out, "a") if a.out else None
+
+    def timeit(fn, pre=None):
+        ts = []
+        for r in range(a.reps + 1):
+            if pre:
+                pre()
+            e0.record(st)
+            fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            if r:
+                ts.append(e0.elapsed_time(e1))
+        return n / (statistics.median(ts) * 1e-3) / 1e9
+
+    def emit(rec):
+        print(json.dumps(rec), flush=True)
+        if fh:
+            fh.write(json.dumps(rec) + "\n")
+
+    for size, m in (("32MB", 1 << 28), ("1GB", 1 << 33)):
+        if m <= (1 << 32):
+            f = bf.Filter(m, 16, 256, 64, bf.BF_CBF)
+            emit({"set": "ablation", "size": size, "step": "gpu_cbf", "add": round(timeit(lambda: f.add(keys), f.clear), 2),
+                  "contains": round(timeit(lambda: f.contains(keys, out)), 2)})
+            del f
+        for scheme, name in ((2, "sbf_iterative"), (1, "sbf_double"), (0, "sbf_multiplicative")):
+            f = bf.Filter(m, 16, 256, 64, "SBF", scheme=scheme)
+            f.set_add_mode(bf.BF_ADD_DIRECT)
+            for lay_name, add_lay, con_lay in (("theta1_kpt1", (1, 4, 1), (1, 4, 1)),
+                                               ("optimised", (4, 1, 4) if scheme != 2 else (1, 4, 1),
+                                                (1, 4, 4) if scheme != 2 else (1, 4, 1))):
+                try:
+                    f.set_layout(0, add_lay[0], add_lay[1], add_lay[2], 0)
+                    f.set_layout(1, con_lay[0], con_lay[1], con_lay[2], 0)
+                except bf.BFError:
+                    continue
+                emit({"set": "ablation", "size": size, "step": name, "layout": lay_name,
+                      "add": round(timeit(lambda: f.add(keys), f.clear), 2),
+                      "contains": round(timeit(lambda: f.contains(keys, out)), 2)})
             del f
 
 
