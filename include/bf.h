@@ -88,7 +88,8 @@ bf_filter* bf_create_seeded(uint64_t m_bits, uint32_t k, uint32_t block_bits,
 /* Bulk insert (P:L245 steps (1)-(2); "the corresponding bits are set to
  * one").  keys: device pointer to n uint64.  Sets the k pattern bits of every
  * key with red.global.or; concurrent bf_add calls on any streams are safe
- * (OR commutes).  Idempotent. */
+ * (OR commutes; binned adds -- bf_set_add_mode -- share the filter's
+ * scratch and are ordered among themselves by the library).  Idempotent. */
 int bf_add(bf_filter* f, const uint64_t* keys, uint64_t n, void* stream);
 
 /* Bulk lookup ("If any bit is zero, the element is certainly not in the
@@ -156,7 +157,12 @@ int bf_set_layout(bf_filter* f, int op, int theta, int phi, int kpt, int hash_va
  * range_bytes / max_batch_keys = 0 choose the defaults (32 MiB, 2^31).
  * BF_EUNSUPPORTED if the binned kernels are not compiled for this
  * configuration and its add schedule. */
-enum { BF_ADD_AUTO = 0, BF_ADD_DIRECT = 1, BF_ADD_BINNED = 2 };
+/*   BF_ADD_HYBRID  direct, but half the warps hand whole-block masks to the
+ *                  TMA engine (cp.reduce.async.bulk .or) while the others
+ *                  use the cooperative red.global.or path: both of the SM's
+ *                  routes to the L2 atomic units at once (NEXT N4; B >= 128,
+ *                  default schedule only). */
+enum { BF_ADD_AUTO = 0, BF_ADD_DIRECT = 1, BF_ADD_BINNED = 2, BF_ADD_HYBRID = 3 };
 int bf_set_add_mode(bf_filter* f, int mode, uint64_t range_bytes, uint64_t max_batch_keys);
 /* mode set by bf_set_add_mode, and whether the most recent bf_add was binned. */
 int bf_get_add_mode(const bf_filter* f, int* mode, int* last_binned);

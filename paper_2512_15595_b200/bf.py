@@ -172,7 +172,7 @@ def bf_get_layout(f: int, op: int) -> dict:
     return dict(zip(("theta", "phi", "kpt", "hash_variant", "specialized"), (int(x.value) for x in v)))
 
 
-BF_ADD_AUTO, BF_ADD_DIRECT, BF_ADD_BINNED = 0, 1, 2
+BF_ADD_AUTO, BF_ADD_DIRECT, BF_ADD_BINNED, BF_ADD_HYBRID = 0, 1, 2, 3
 
 
 def bf_set_add_mode(f: int, mode: int, range_bytes: int = 0, max_batch_keys: int = 0) -> None:

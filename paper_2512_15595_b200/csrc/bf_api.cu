@@ -143,6 +143,12 @@ struct bf_filter {
     uint32_t nparts, part;
     uint64_t b_global, blk_lo, blk_hi;
     uint32_t* bounds;  // device: nparts + 1 block boundaries
+    // the binned-add scratch and the host-path staging buffers are shared by
+    // every call on this filter: a host mutex serialises their (re)use, and
+    // scratch_done (recorded after each binned add) orders the device work of
+    // binned adds issued on different streams
+    std::mutex mu;
+    cudaEvent_t scratch_done;
 };
 
 static int validate(uint64_t m_bits, uint32_t k, uint32_t B, uint32_t S, uint32_t variant, uint32_t* z_out)
@@ -364,6 +370,7 @@ void bf_destroy(bf_filter* f)
     if (f->recs) cudaFree(f->recs);
     if (f->cursor) cudaFree(f->cursor);
     if (f->bounds) cudaFree(f->bounds);
+    if (f->scratch_done) cudaEventDestroy(f->scratch_done);
     cudaFree(f->words);
     delete f;
 }
@@ -464,8 +471,28 @@ static bool binned_available(const bf_filter* f, KernelFn* bin, KernelFn* apply)
     return *bin && *apply;
 }
 
+static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cudaStream_t st, KernelFn bin_fn,
+                             KernelFn apply_fn);
+
 static int binned_add(bf_filter* f, const uint64_t* keys, uint64_t n, cudaStream_t st, KernelFn bin_fn,
                       KernelFn apply_fn)
+{
+    std::lock_guard<std::mutex> g(f->mu);
+    cudaError_t e = cudaSuccess;
+    if (!f->scratch_done) {
+        if ((e = cudaEventCreateWithFlags(&f->scratch_done, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(e, "binned add: event");
+    } else if ((e = cudaStreamWaitEvent(st, f->scratch_done, 0)) != cudaSuccess) {
+        return cuda_fail(e, "binned add: wait for the previous binned add");
+    }
+    int rc = binned_add_locked(f, keys, n, st, bin_fn, apply_fn);
+    if (rc == BF_OK && (e = cudaEventRecord(f->scratch_done, st)) != cudaSuccess)
+        return cuda_fail(e, "binned add: event record");
+    return rc;
+}
+
+static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cudaStream_t st, KernelFn bin_fn,
+                             KernelFn apply_fn)
 {
     const uint64_t blk_bytes = f->B / 8;
     uint64_t range_bytes = f->range_bytes ? f->range_bytes : kDefaultRangeBytes;
@@ -544,9 +571,20 @@ static int binned_add(bf_filter* f, const uint64_t* keys, uint64_t n, cudaStream
     return BF_OK;
 }
 
+static KernelFn hybrid_kernel(const bf_filter* f)
+{
+    const Sched& sc = f->sched[0];
+    if (!sc.specialized || f->scheme != 0) return nullptr;
+    InstKey kh{5, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z,
+               (uint8_t)sc.theta, (uint8_t)sc.phi, (uint8_t)sc.kpt, (uint8_t)sc.hv};
+    return registry_find(kh);
+}
+
 int bf_set_add_mode(bf_filter* f, int mode, uint64_t range_bytes, uint64_t max_batch_keys)
 {
-    if (!f || mode < BF_ADD_AUTO || mode > BF_ADD_BINNED) return fail(BF_EINVAL, "bad filter or add mode");
+    if (!f || mode < BF_ADD_AUTO || mode > BF_ADD_HYBRID) return fail(BF_EINVAL, "bad filter or add mode");
+    if (mode == BF_ADD_HYBRID && !hybrid_kernel(f))
+        return fail(BF_EUNSUPPORTED, "hybrid add is not compiled for this configuration / add schedule");
     if (range_bytes && range_bytes < (uint64_t)f->B / 8) return fail(BF_EINVAL, "range_bytes smaller than a block");
     if (mode == BF_ADD_BINNED) {
         KernelFn a, b;
@@ -583,6 +621,21 @@ int bf_add(bf_filter* f, const uint64_t* keys, uint64_t n, void* stream)
         return binned_add(f, keys, n, (cudaStream_t)stream, bin_fn, apply_fn);
     }
     f->last_add_binned = 0;
+    if (f->add_mode == BF_ADD_HYBRID) {
+        KernelFn hy = hybrid_kernel(f);
+        if (hy) {
+            const uint64_t tiles = (n + 32ULL * f->sched[0].kpt - 1) / (32ULL * f->sched[0].kpt);
+            uint64_t grid = (tiles + 7) / 8;
+            const int maxg = pick_grid(f, hy);
+            if (grid > (uint64_t)maxg) grid = maxg;
+            Params p = make_params(f, keys, n, nullptr);
+            void* args[] = {&p};
+            cudaError_t e = cudaLaunchKernel((const void*)hy, dim3((unsigned)(grid ? grid : 1)), dim3(256), args, 0,
+                                             (cudaStream_t)stream);
+            if (e != cudaSuccess) return cuda_fail(e, "hybrid add launch");
+            return check_launch("hybrid add launch");
+        }
+    }
     return launch_bulk(f, 0, keys, n, nullptr, (cudaStream_t)stream);
 }
 
@@ -750,6 +803,7 @@ static int ensure_staging(bf_filter* f)
 
 static int host_bulk(bf_filter* f, int op, const uint64_t* hkeys, uint64_t n, uint32_t* hout, cudaStream_t st)
 {
+    std::lock_guard<std::mutex> g(f->mu);  // one host-path call at a time per filter (shared staging)
     int rc = ensure_staging(f);
     if (rc) return rc;
     cudaError_t e = cudaSuccess;

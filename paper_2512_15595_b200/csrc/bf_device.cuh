@@ -211,7 +211,7 @@ template <int I, int N> struct StaticFor {
     }
 };
 
-constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
 
 // Spread the low 8 bits of x to every 4th bit (bit i -> bit 4i).
 __device__ __forceinline__ uint32_t spread4(uint32_t x)

@@ -520,4 +520,120 @@ __global__ void __launch_bounds__(256) bulk_kernel(const Params p)
     }
 }
 
+// ----------------------------------------------------------------- hybrid add
+// Bulk add that drives BOTH of the SM's paths to L2 atomics (NEXT N4): even
+// warps run the cooperative LSU kernel above (Θ=s lanes, red.global.or per
+// word), odd warps have each lane build its keys' whole block masks in shared
+// memory and hand them to the TMA engine (cp.reduce.async.bulk .or.b64 of
+// the block).  The LSU path is capped by the L1->XBAR request path (~1 sector
+// RED per 2 clocks per SM), the TMA path bypasses L1; measured probe rates
+// (profiles/r1_n4_tma_probe.jsonl): B=256 119.6 (LSU) / 81 (TMA) / 127
+// (both), B=512 75 / 72 / 101.5, B=1024 38 / 49.5 / 64 G blocks/s.  Same
+// bits as every other add schedule.
+template <class C>
+__global__ void __launch_bounds__(256) hybrid_add_kernel(const Params p)
+{
+    using W = typename C::W;
+    // Θ = 1 view of the same filter for the TMA lanes' salts (immediates)
+    using C1 = Cfg<C::V, C::S, ilog2(C::s), C::K, C::Z, 1, C::s, C::KPT, 0>;
+    constexpr int KPT = C::KPT;
+    constexpr uint32_t BLK = C::B / 8;  // bytes per block (>= 16 for the bulk op)
+    // per-lane double buffer of a tile's KPT block masks (one fence and one
+    // bulk group per tile); KPT_T keys per TMA-lane tile keep it <= 32 KB
+    constexpr int KPT_T = (2 * KPT * 128 * BLK <= 32768) ? KPT : (32768 / (2 * 128 * BLK) >= 1 ? 32768 / (2 * 128 * BLK) : 1);
+    static_assert(BLK >= 16 && KPT % KPT_T == 0, "hybrid add needs 16..256-byte blocks");
+    __shared__ __align__(128) W s_mask[128][2][KPT_T][C::s];
+
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const bool tma_warp = warp & 1u;
+    constexpr uint64_t TILE = 32 * KPT;
+    const uint64_t ntiles = (p.n + TILE - 1) / TILE;
+    const uint64_t nfull = p.n / TILE;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const bool vec_ok = (((uintptr_t)p.keys) & (8 * KPT - 1)) == 0;
+
+    if (!tma_warp) {  // LSU path: the cooperative kernel's tile loop over this warp's tiles
+        const uint32_t pos = lane & (uint32_t)(C::THETA - 1);
+        const uint32_t gbase = lane & ~(uint32_t)(C::THETA - 1);
+        SaltSrc<C> ss;
+        ss.init(pos, nullptr, nullptr);
+        uint64_t kcur[KPT] = {};
+        uint64_t knext[KPT];
+        if (gw < nfull) load_tile_keys<KPT>(p.keys, gw * TILE + lane * KPT, vec_ok, kcur);
+        for (uint64_t t = gw; t < ntiles; t += nw) {
+            const uint64_t tn = t + nw;
+            const bool have_next = tn < nfull;
+            if (t < nfull)
+                run_tile<C, true, true>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
+                                        tn * TILE + lane * KPT);
+            else
+                run_tile<C, true, false>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
+                                         tn * TILE + lane * KPT);
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) kcur[j] = knext[j];
+        }
+        return;
+    }
+    // TMA path: each lane owns its keys; masks -> shared -> bulk OR
+    SaltSrc<C1> ss1;
+    ss1.init(0, nullptr, nullptr);
+    const uint32_t slot = (warp >> 1) * 32 + lane;  // 0..127
+    W* F = (W*)p.words;
+    uint32_t it = 0;  // tiles done by this warp
+    for (uint64_t t = gw; t < ntiles; t += nw, ++it) {
+        const uint64_t mine = t * TILE + (uint64_t)lane * KPT;
+        uint64_t key[KPT];
+        bool valid[KPT];
+        if (t < nfull) {
+            load_tile_keys<KPT>(p.keys, mine, vec_ok, key);
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) valid[j] = true;
+        } else {
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) {
+                valid[j] = mine + j < p.n;
+                key[j] = valid[j] ? ld_key1(p.keys + mine + j) : 0ULL;
+            }
+        }
+        uint32_t blk[KPT];
+#pragma unroll
+        for (int j0 = 0; j0 < KPT; j0 += KPT_T) {
+            const uint32_t r = (it * (KPT / KPT_T) + j0 / KPT_T) & 1;
+            // the bulk group that last read buffer r (two groups ago) is done reading it
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+#pragma unroll
+            for (int jj = 0; jj < KPT_T; ++jj) {
+                const int j = j0 + jj;
+                const uint64_t h = xxh64_u64(key[j], p.seed);
+                blk[j] = block_of(h, p.b32);
+                const Draws<C1> dr((uint32_t)h);
+                StaticFor<0, C::s>::run([&](auto I) {
+                    s_mask[slot][r][jj][decltype(I)::value] =
+                        slot_mask<C1, decltype(I)::value>(dr, decltype(I)::value, ss1);
+                });
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+            for (int jj = 0; jj < KPT_T; ++jj) {
+                const int j = j0 + jj;
+                if (!valid[j]) continue;
+                const uint32_t src = (uint32_t)__cvta_generic_to_shared(&s_mask[slot][r][jj][0]);
+                if constexpr (C::S == 64)
+                    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.or.b64 [%0], [%1], %2;" ::"l"(
+                                     F + (uint64_t)blk[j] * C::s),
+                                 "r"(src), "n"(BLK)
+                                 : "memory");
+                else
+                    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.or.b32 [%0], [%1], %2;" ::"l"(
+                                     F + (uint64_t)blk[j] * C::s),
+                                 "r"(src), "n"(BLK)
+                                 : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 }  // namespace bf

@@ -143,6 +143,8 @@ def emit():
             binned.append((2, v, B, S, k, z, 1, 1, 1, 0))
             binned.append((3, v, B, S, k, z, theta, phi, kpt, hv))
             binned.append((4, v, B, S, k, z, 1, B // S, 1, 0))  # routed contains (Θ=1, Φ=s)
+            if B >= 128:
+                binned.append((5, v, B, S, k, z, theta, phi, kpt, hv))  # hybrid TMA+LSU add
     inst = inst + binned + scheme_instances()
     shards = [inst[i::NSHARDS] for i in range(NSHARDS)]
     for si, sh in enumerate(shards):
@@ -158,6 +160,8 @@ def emit():
                 fn = f"apply_kernel<{cfg_type(i)}>"
             elif op == 4:
                 fn = f"contains_bucket_kernel<{cfg_type(i)}>"
+            elif op == 5:
+                fn = f"hybrid_add_kernel<{cfg_type(i)}>"
             else:
                 fn = f"bulk_kernel<{cfg_type(i)}, {'true' if op == 0 else 'false'}>"
             lines.append(f"    registry_add(InstKey{{{op}, {v}, {B}, {S}, {k}, {z}, {theta}, {phi}, {kpt}, {hv}, {hs}}}, "

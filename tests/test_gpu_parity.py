@@ -539,3 +539,90 @@ def test_draw_schemes_match_oracle(bflib, cuda, cfg, scheme):
         assert np.array_equal(_gpu_bytes(f), o.bytes()), (op, th, ph, kpt)
     f.set_layout(1, 1, s, 1 if scheme == 2 else 4, 0)
     assert np.array_equal(_gpu_contains(torch, f, qd), o.contains(q))
+
+
+def test_concurrent_binned_adds_and_host_calls(bflib, cuda):
+    """Binned adds on two streams from two host threads share the filter's
+    scratch: the library orders them; the result is the oracle's filter.
+    Host-buffer calls from two threads are serialised per filter."""
+    import threading
+
+    import torch
+    bf = bflib
+    m = 1 << 24
+    keys = synth.keys(31, 400_000)
+    o = OracleFilter(3, m, B=256, S=64, k=8)
+    o.add(keys, threads=8)
+    f = bf.Filter(m, 8, 256, 64, "SBF")
+    f.set_add_mode(bf.BF_ADD_BINNED, 1 << 16, 50_000)
+    halves = [_to_dev(torch, keys[:200_000], cuda), _to_dev(torch, keys[200_000:], cuda)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+
+    def work(i):
+        with torch.cuda.stream(streams[i]):
+            f.add(halves[i])
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    torch.cuda.synchronize()
+    assert np.array_equal(_gpu_bytes(f), o.bytes())
+
+    g = bf.Filter(m, 8, 256, 64, "SBF")
+    hk = [torch.from_numpy(keys[:200_000].view(np.int64)).pin_memory(),
+          torch.from_numpy(keys[200_000:].view(np.int64)).pin_memory()]
+    th = [threading.Thread(target=lambda i=i: g.add_host(hk[i])) for i in range(2)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    torch.cuda.synchronize()
+    assert np.array_equal(_gpu_bytes(g), o.bytes())
+
+
+def test_max_block_count_2pow32(bflib, cuda):
+    """b = 2^32 blocks (the largest filter the spec allows; block = h >> 32,
+    the b mod 2^32 == 0 path): RBBF 32/32, a 16 GiB filter; sampled block
+    ranges equal the oracle's and every inserted key is found."""
+    import torch
+    bf = bflib
+    m = 1 << 37  # 2^32 blocks of 32 bits
+    free, _ = torch.cuda.mem_get_info()
+    if free < (m // 8) + (1 << 30):
+        pytest.skip("not enough device memory")
+    n = 1 << 22
+    kd = torch.empty(n, dtype=torch.int64, device=cuda)
+    bf.bf_keygen(kd, n, 99)
+    f = bf.Filter(m, 5, 32, 32, "RBBF")
+    assert f.b == 1 << 32
+    f.add(kd)
+    out = f.contains(kd)
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy().view(np.uint32) == 0xFFFFFFFF).all()
+    keys = synth.keys(99, n)
+    o = OracleFilter(2, m, B=32, S=32, k=5, allocate=False)
+    data = f.data()
+    for lo in (0, (1 << 31) + 12345, (1 << 32) - 8192):
+        hi = lo + 8192
+        assert np.array_equal(data[lo * 4: hi * 4].cpu().numpy(), o.add_range(keys, lo, hi, threads=os.cpu_count())), lo
+
+
+HYBRID_CFGS = [(3, 256, 64, 8, 0), (3, 256, 32, 16, 0), (1, 256, 64, 8, 0), (4, 256, 32, 8, 2), (3, 128, 64, 8, 0),
+               (3, 512, 64, 16, 0), (3, 1024, 64, 16, 0), (4, 1024, 64, 16, 4)]
+
+
+@pytest.mark.parametrize("cfg", HYBRID_CFGS)
+def test_hybrid_add_matches_oracle(bflib, cuda, cfg):
+    """BF_ADD_HYBRID (half the warps OR whole blocks through the TMA engine,
+    half through cooperative red.global.or) builds the oracle's filter."""
+    import torch
+    bf = bflib
+    v, B, S, k, z = cfg
+    m = B * 20_011
+    keys = synth.keys(41, 150_001)
+    o = OracleFilter(v, m, B=B, S=S, k=k, z=z)
+    o.add(keys, threads=4)
+    f = bf.Filter(m, k, B, S, variant=v, z=z)
+    f.set_add_mode(bf.BF_ADD_HYBRID)
+    f.add(_to_dev(torch, keys, cuda))
+    torch.cuda.synchronize()
+    assert np.array_equal(_gpu_bytes(f), o.bytes())
