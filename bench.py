@@ -274,6 +274,9 @@ def run_ours(a, cfg, rank, world, local_rank):
     t_con = statistics.mean(e[3].elapsed_time(e[4]) for e in evs)
     t_merge = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
     t_clear = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    per_step = [e[0].elapsed_time(e[4]) for e in evs]
+    rel_stderr = (statistics.stdev(per_step) / statistics.mean(per_step) / len(per_step) ** 0.5
+                  if len(per_step) > 1 else None)
     ms = ms_local
     if world > 1:
         tt = torch.tensor([ms_local], device=dev)
@@ -315,10 +318,12 @@ def run_ours(a, cfg, rank, world, local_rank):
         lay = f.layout(0 if dominant == "add" else 1)
         vid = VARIANT_IDS[cfg["variant"]]
         lgs = (cfg["B"] // cfg["S"]).bit_length() - 1
-        sig = (f"Cfg<{vid}, {cfg['S']}, {lgs}, {cfg['k']}, {cfg['z']}, {lay['theta']}, {lay['phi']}, "
-               f"{lay['kpt']}, {lay['hash_variant']}>, {1 if dominant == 'add' else 0}>")
+        head = (f"Cfg<{vid}, {cfg['S']}, {lgs}, {cfg['k']}, {cfg['z']}, {lay['theta']}, {lay['phi']}, "
+                f"{lay['kpt']}, {lay['hash_variant']}")
+        tail = f">, {1 if dominant == 'add' else 0}>"
+        sigs = (head + tail, head + ", 0" + tail)  # with / without the default draw-scheme argument
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        hit = [v for k, v in tr["kernels"].items() if sig in k and v.get("n") == n]
+        hit = [v for k, v in tr["kernels"].items() if any(sg in k for sg in sigs) and v.get("n") == n]
         if hit:
             roofline["traffic"] = hit[0]["dram_bytes_per_launch"]
             roofline["traffic_source"] = tr.get("source")
@@ -345,6 +350,7 @@ def run_ours(a, cfg, rank, world, local_rank):
         "contains_gkeys_s": round(n / (t_con * 1e-3) / 1e9, 3),
         "kernel_ms": {"clear": round(t_clear, 4), "add": round(t_add, 4), "merge": round(t_merge, 4),
                       "contains": round(t_con, 4)},
+        "step_rel_stderr": round(rel_stderr, 5) if rel_stderr is not None else None,
         "roofline": roofline,
         "gpu_launches": launches,
         "clocks": clk.summary(),

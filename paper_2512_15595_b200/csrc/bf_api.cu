@@ -696,11 +696,14 @@ int bf_route(const bf_filter* f, const uint64_t* keys, uint64_t n, uint64_t idx_
     bp.idx_out = idx;
     bp.idx_base = idx_base;
     static uint32_t* zero_bounds[64] = {nullptr};  // P == 1: every block is owned by part 0
+    static std::mutex zero_mu;
     if (!bp.bounds) {
-        int dev = f->device;
+        const int dev = f->device;
+        if (dev < 0 || dev >= 64) return fail(BF_EINVAL, "device index out of range");
+        std::lock_guard<std::mutex> lk(zero_mu);
         if (!zero_bounds[dev]) {
             if ((e = cudaMalloc(&zero_bounds[dev], 2 * sizeof(uint32_t))) != cudaSuccess) return cuda_fail(e, "bounds");
-            cudaMemset(zero_bounds[dev], 0, 2 * sizeof(uint32_t));
+            if ((e = cudaMemset(zero_bounds[dev], 0, 2 * sizeof(uint32_t))) != cudaSuccess) return cuda_fail(e, "bounds");
         }
         bp.bounds = zero_bounds[dev];
     }
