@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="time eager launches instead of replays of one captured step (CUDA graph, N=1 default)")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
     cfg = dict(CONFIGS[a.config])
@@ -261,14 +263,35 @@ def run_ours(a, cfg, rank, world, local_rank):
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(a.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    graph = None
+    if a.graph and world == 1:
+        # per-kernel times from eager steps, then the timed region replays one
+        # captured step (launch overhead removed: matters for small batches)
+        for i in range(a.steps):
+            step(evs[i])
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(graph, stream=cap):
+                step()
+        stream.wait_stream(cap)
+        graph.replay()
+        torch.cuda.synchronize()
     launches0 = bf.bf_launch_count()
     with ClockSampler(local_rank) as clk:
         t_start.record(stream)
         for i in range(a.steps):
-            step(evs[i])
+            if graph is not None:
+                graph.replay()
+            else:
+                step(evs[i])
         t_end.record(stream)
         torch.cuda.synchronize()
     launches = bf.bf_launch_count() - launches0
+    if graph is not None:
+        launches = 2 * a.steps  # the graph replays the two captured kernels per step
     ms_local = t_start.elapsed_time(t_end) / a.steps
     t_add = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
     t_con = statistics.mean(e[3].elapsed_time(e[4]) for e in evs)
@@ -344,6 +367,7 @@ def run_ours(a, cfg, rank, world, local_rank):
                    "merge": a.merge if world > 1 else None,
                    "layout_add": f.layout(0), "layout_contains": f.layout(1),
                    "add_path": "binned" if f.add_mode()[1] else "direct",
+                   "cuda_graph": graph is not None,
                    "l2": f"inputs larger than L2 ({n * 8 >> 20} MiB keys streamed per kernel); "
                          f"filter {cfg['residency']}-resident by design"},
         "add_gkeys_s": round(n / (t_add * 1e-3) / 1e9, 3),
