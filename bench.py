@@ -8,6 +8,7 @@ One step = one pass of the whole hot path over one batch of synthetic keys
 resident in HBM (BASELINE.json configs[1] by default: a 32 MiB L2-resident
 filter, 2^26 uniform unique uint64 keys):
     bf_clear -> bf_add(2^26 keys) -> [N>1: OR-merge of the partial filters]
+             (N=1: the step is captured once in a CUDA graph and replayed)
              -> bf_contains(the same 2^26 keys; all true)
 value = keys processed by add + contains over all ranks / max-over-ranks time.
 
@@ -210,9 +211,29 @@ def cpu_baseline(cfg):
     f.add(keys, threads=cores)
     f.contains(keys, threads=cores)
     t = time.perf_counter() - t0
+    # one thread (T=1 and T=all host cores), a 2^22-key sample
+    s1 = min(sample, 1 << 22)
+    g = OracleFilter(v, cfg["m_bits"], B=cfg["B"], S=cfg["S"], k=cfg["k"], z=cfg["z"])
+    t1 = time.perf_counter()
+    g.add(keys[:s1], threads=1)
+    g.contains(keys[:s1], threads=1)
+    t1 = time.perf_counter() - t1
     return {"value": 2 * sample / t / 1e9, "unit": "Gkeys/s", "cores": cores, "kind": "oracle",
             "sample": f"add {sample} + contains {sample} keys of the same workload (full-size filter), "
-                      f"{t:.2f} s on {cores} threads"}
+                      f"{t:.2f} s on {cores} threads",
+            "single_thread": {"value": 2 * s1 / t1 / 1e9, "unit": "Gkeys/s",
+                              "sample": f"add {s1} + contains {s1} keys, {t1:.2f} s on 1 thread"},
+            "host_cpu": _cpu_model()}
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # --------------------------------------------------------------------- ours

@@ -626,3 +626,33 @@ def test_hybrid_add_matches_oracle(bflib, cuda, cfg):
     f.add(_to_dev(torch, keys, cuda))
     torch.cuda.synchronize()
     assert np.array_equal(_gpu_bytes(f), o.bytes())
+
+
+def test_cuda_graph_capture_and_replay(bflib, cuda):
+    """bf_clear + bf_add + bf_contains are stream-ordered and capture-safe:
+    one captured step replayed three times gives the oracle's bits and
+    answers (bench.py times such replays)."""
+    import torch
+    bf = bflib
+    n = (1 << 18) + 7
+    keys = synth.keys(3, n)
+    o = OracleFilter(3, 1 << 22, B=256, S=64, k=8)
+    o.add(keys)
+    f = bf.Filter(1 << 22, 8, 256, 64, "SBF")
+    kd = _to_dev(torch, keys, cuda)
+    out = torch.empty((n + 31) // 32, dtype=torch.int32, device=cuda)
+    f.add(kd)  # warm-up (lazy module loading) outside the capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            f.clear()
+            f.add(kd)
+            f.contains(kd, out)
+    for _ in range(3):
+        out.fill_(0)
+        g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(_gpu_bytes(f), o.bytes())
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), o.contains(keys))
