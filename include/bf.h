@@ -248,6 +248,48 @@ int bf_probe_red(void* buf, uint64_t b, uint32_t block_bits, uint32_t lanes,
 int bf_probe_rng(void* buf, uint64_t b, uint32_t block_bits, int red, uint32_t lanes, uint64_t n,
                  void* stream);
 
+/* ---- In-switch OR merge over NVLink SHARP ----
+ *
+ * Merging P partial filters built on P GPUs ("insertions ...
+ * parallel ... combined") is a bitwise OR of P equal-sized bit arrays.  On an
+ * NVSwitch system the switch can do that OR itself: every rank binds one
+ * physical buffer of its own to a shared multicast object; rank r then reads
+ * words [r*W/P, (r+1)*W/P) through the multicast address with
+ * multimem.ld_reduce.or.b64 (the switch returns the OR of all P copies) and
+ * stores the result with multimem.st.b64 (the switch writes it into all P
+ * copies).  After every rank's reduce completes, every copy holds the OR.
+ *
+ * Protocol (collective over the P ranks, one GPU per process, the caller's
+ * current device):
+ *   1. rank 0: bf_mcast_create(bytes, P, type, 1, handle, &m) fills the
+ *      BF_MCAST_HANDLE_BYTES-byte `handle` blob; broadcast it;
+ *   2. ranks 1..P-1: bf_mcast_create(bytes, P, type, 0, handle, &m) imports;
+ *   3. every rank: bf_mcast_add_device(m); barrier (all devices must be
+ *      added before any memory is bound);
+ *   4. every rank: bf_mcast_bind(m, &uc) allocates this rank's copy (size
+ *      rounded up to the multicast granularity, bf_mcast_mc_ptr reports it)
+ *      and returns its ordinary device pointer `uc`; barrier;
+ *   5. per merge: write the partial filter into `uc` (any stream), sync,
+ *      barrier; bf_mcast_or_reduce(m, rank, bytes, stream); sync, barrier;
+ *      `uc` now holds the OR of all P partial filters (bytes % 8 == 0);
+ *   6. bf_mcast_destroy(m) (after a final barrier).
+ * type: BF_MCAST_POSIX_FD (single node; the blob carries the exporter's pid
+ * and fd, importers duplicate it with pidfd_getfd) or BF_MCAST_FABRIC (IMEX
+ * fabric handle).  Returns BF_EUNSUPPORTED where the device or driver has no
+ * multicast; driver failures return BF_ECUDA with the driver's message.
+ * The multicast object and all memory belong to the handle. */
+#define BF_MCAST_POSIX_FD 0
+#define BF_MCAST_FABRIC 1
+#define BF_MCAST_HANDLE_BYTES 64
+typedef struct bf_mcast bf_mcast; /* opaque */
+int bf_mcast_create(uint64_t bytes, uint32_t nranks, int handle_type, int exporter, void* handle,
+                    bf_mcast** out);
+int bf_mcast_add_device(bf_mcast* m);
+int bf_mcast_bind(bf_mcast* m, void** uc_ptr);
+int bf_mcast_mc_ptr(bf_mcast* m, void** mc_ptr, uint64_t* size);
+int bf_mcast_or_reduce(bf_mcast* m, uint32_t rank, uint64_t bytes, void* stream);
+void bf_mcast_destroy(bf_mcast* m);
+
 /* Number of kernels this library has launched since load (all entry points).
  * Lets callers prove the CUDA path ran. */
 uint64_t bf_launch_count(void);

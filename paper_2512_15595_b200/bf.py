@@ -67,6 +67,12 @@ _SIGS = {
     "bf_add_routed": (_i32, [_vp, _vp, _vp, _u32, _u64, _vp]),
     "bf_contains_routed": (_i32, [_vp, _vp, _vp, _u32, _u64, _vp, _vp]),
     "bf_scatter_results": (_i32, [_vp, _vp, _vp, _u32, _u64, _vp, _vp]),
+    "bf_mcast_create": (_i32, [_u64, _u32, _i32, _i32, _vp, C.POINTER(_vp)]),
+    "bf_mcast_add_device": (_i32, [_vp]),
+    "bf_mcast_bind": (_i32, [_vp, C.POINTER(_vp)]),
+    "bf_mcast_mc_ptr": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_u64)]),
+    "bf_mcast_or_reduce": (_i32, [_vp, _u32, _u64, _vp]),
+    "bf_mcast_destroy": (None, [_vp]),
     "bf_launch_count": (_u64, []),
     "bf_last_error": (C.c_char_p, [C.POINTER(_i32)]),
     "bf_version": (C.c_char_p, []),
@@ -240,6 +246,43 @@ def bf_contains_routed(f: int, recs, counts, nsrc: int, cap: int, res, stream=No
 
 def bf_scatter_results(idx, res, counts, nsrc: int, cap: int, out_bits, stream=None) -> None:
     _check(_lib.bf_scatter_results(_ptr(idx), _ptr(res), _ptr(counts), nsrc, cap, _ptr(out_bits), _stream(stream)))
+
+
+BF_MCAST_POSIX_FD, BF_MCAST_FABRIC, BF_MCAST_HANDLE_BYTES = 0, 1, 64
+
+
+def bf_mcast_create(nbytes: int, nranks: int, handle_type: int, exporter: bool,
+                    handle: bytes | None = None) -> tuple[int, bytes]:
+    """Returns (mcast handle, 64-byte shareable blob).  Importers pass the
+    exporter's blob."""
+    blob = C.create_string_buffer(handle or b"", BF_MCAST_HANDLE_BYTES)
+    out = _vp()
+    _check(_lib.bf_mcast_create(nbytes, nranks, handle_type, int(bool(exporter)), blob, C.byref(out)))
+    return out.value, blob.raw
+
+
+def bf_mcast_add_device(m: int) -> None:
+    _check(_lib.bf_mcast_add_device(m))
+
+
+def bf_mcast_bind(m: int) -> int:
+    p = _vp()
+    _check(_lib.bf_mcast_bind(m, C.byref(p)))
+    return p.value
+
+
+def bf_mcast_mc_ptr(m: int) -> tuple[int, int]:
+    p, n = _vp(), _u64()
+    _check(_lib.bf_mcast_mc_ptr(m, C.byref(p), C.byref(n)))
+    return p.value, int(n.value)
+
+
+def bf_mcast_or_reduce(m: int, rank: int, nbytes: int, stream=None) -> None:
+    _check(_lib.bf_mcast_or_reduce(m, rank, nbytes, _stream(stream)))
+
+
+def bf_mcast_destroy(m: int) -> None:
+    _lib.bf_mcast_destroy(m)
 
 
 def bf_launch_count() -> int:

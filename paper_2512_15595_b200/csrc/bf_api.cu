@@ -74,6 +74,12 @@ static int check_launch(const char* what)
     return BF_OK;
 }
 
+int report_error(int code, const char* what, const char* detail)
+{
+    return fail(code, "%s: %s", what, detail);
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 // device guard: run on the filter's device, restore the caller's afterwards
 struct DeviceGuard {
     int prev = -1;

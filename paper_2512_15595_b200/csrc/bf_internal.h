@@ -44,6 +44,10 @@ void launch_probe_rng(const void* buf, uint64_t b, uint32_t B, int red, uint32_t
 void launch_scatter_results(const uint64_t* idx, const uint8_t* res, const unsigned long long* counts,
                             uint32_t nsrc, uint64_t cap, uint32_t* out_bits, cudaStream_t st, int grid);
 
+// error slot / launch counter of bf_api.cu, for the other C-ABI units
+int report_error(int code, const char* what, const char* detail);
+void count_launch();
+
 struct Registrar {
     Registrar(void (*fn)()) { fn(); }
 };

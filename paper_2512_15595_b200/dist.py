@@ -76,7 +76,75 @@ def merge_alltoall(words: torch.Tensor, group=None, or_fold=gpu_or_fold) -> None
         words.copy_(send[:M])
 
 
-MERGES = {"allgather": merge_allgather, "alltoall": merge_alltoall}
+class NvlsMerger:
+    """E4: in-switch OR merge over NVLink SHARP (bf_mcast_*, include/bf.h).
+
+    Collective constructor: rank 0 creates the multicast object and
+    broadcasts its handle, every rank adds its device and binds a
+    ``nbytes`` buffer of its own (``self.buf``, a uint8 device view).
+    ``merge(words)``: copy the partial filter in, each rank ORs its 1/P slice
+    of all copies inside the switch (multimem.ld_reduce.or + multimem.st),
+    copy the merged filter back.  NVLink traffic per rank: M/P in + M/P out
+    through the switch, against 2(P-1)/P*M for E2."""
+
+    def __init__(self, nbytes: int, group=None, handle_type: int | None = None):
+        from . import bf
+        self.group = group
+        self.P = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        ht = bf.BF_MCAST_POSIX_FD if handle_type is None else handle_type
+        obj = [None]
+        if self.rank == 0:
+            self.m, blob = bf.bf_mcast_create(nbytes, self.P, ht, True)
+            obj = [blob]
+        if self.P > 1:
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+        if self.rank != 0:
+            self.m, _ = bf.bf_mcast_create(nbytes, self.P, ht, False, obj[0])
+        bf.bf_mcast_add_device(self.m)
+        self._barrier()
+        uc = bf.bf_mcast_bind(self.m)
+        self._barrier()
+        self.nbytes = nbytes
+        self.buf = bf._device_view(uc, nbytes)
+
+    def _barrier(self):
+        if self.P > 1:
+            dist.barrier(group=self.group)
+
+    def merge(self, words: torch.Tensor) -> None:
+        from . import bf
+        M = words.numel()
+        assert M <= self.nbytes and M % 8 == 0
+        self.buf[:M].copy_(words)
+        torch.cuda.synchronize()
+        self._barrier()
+        bf.bf_mcast_or_reduce(self.m, self.rank, M)
+        torch.cuda.synchronize()
+        self._barrier()
+        words.copy_(self.buf[:M])
+
+    def close(self):
+        from . import bf
+        if getattr(self, "m", None):
+            self._barrier()
+            bf.bf_mcast_destroy(self.m)
+            self.m = None
+
+
+_nvls_cache: dict = {}
+
+
+def merge_nvls(words: torch.Tensor, group=None) -> None:
+    """E4 as a MERGES entry: one NvlsMerger per (group, size), kept for reuse."""
+    key = (id(group), words.numel(), words.device.index)
+    mg = _nvls_cache.get(key)
+    if mg is None:
+        mg = _nvls_cache[key] = NvlsMerger(words.numel(), group)
+    mg.merge(words)
+
+
+MERGES = {"allgather": merge_allgather, "alltoall": merge_alltoall, "nvls": merge_nvls}
 
 
 def build_replicated(filt, keys: torch.Tensor, strategy: str = "alltoall", group=None) -> None:
