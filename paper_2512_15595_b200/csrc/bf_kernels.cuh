@@ -65,6 +65,17 @@ struct Cfg {
     // flight only when the KPT loaded blocks leave room for them
     // (KPT*s*S/32 registers); add and cooperative contains always do
     static constexpr bool PREFETCH_T1 = (KPT * s * S / 32 <= 16);
+    // BBF contains (Θ = 1) with B >= 256 tests its draws against a copy of
+    // the block in shared memory instead of selecting the word among s
+    // registers (a SEL chain of s-1 steps per draw): per-CTA staging of
+    // 8 warps x KPT keys x B/32 words x 32 lanes, <= 32 KB
+    static constexpr int BBF_SM_WORDS = 8 * KPT * (B / 32) * 32;
+    static constexpr bool BBF_SM = (V == V_BBF) && (B >= 256) && (BBF_SM_WORDS <= 8192);
+    // BBF add (Θ > 1) with B >= 256: each lane ORs its own keys' whole
+    // patterns into shared memory (one atomic per draw) and the group then
+    // issues the coalesced REDs from there, instead of every lane of the group
+    // evaluating all k draws against its own words (Θ-fold redundant work)
+    static constexpr bool BBF_SMA = (V == V_BBF) && (THETA > 1) && (B >= 256) && (BBF_SM_WORDS <= 8192);
     using W = typename WordT<S>::T;
 
     static_assert(S == 32 || S == 64, "word size");
@@ -282,6 +293,31 @@ __device__ __forceinline__ bool test_block(const typename C::W* wd, const Draws<
     return acc & 1u;
 }
 
+// BBF contains on a loaded block staged through shared memory (Cfg::BBF_SM).
+// `col` is this lane's column of its key slot: 32-bit word q of the block at
+// col[q*32], so a warp's accesses hit 32 distinct banks whatever words its
+// lanes' draws select.  Bit p of the block is bit (p & 31) of word p >> 5
+// (little-endian words): one LDS and one funnel rotate
+// per draw.  Each lane reads only what it wrote (program order, no barrier).
+template <class C>
+__device__ __forceinline__ bool test_block_sm(const typename C::W* wd, const Draws<C>& dr, const SaltSrc<C>& ss,
+                                              uint32_t* col)
+{
+    constexpr int NW32 = C::B / 32;
+#pragma unroll
+    for (int q = 0; q < NW32; ++q) {
+        if constexpr (C::S == 64) col[q * 32] = (uint32_t)(wd[q >> 1] >> (32 * (q & 1)));
+        else col[q * 32] = (uint32_t)wd[q];
+    }
+    uint32_t acc = 0xffffffffu;
+    StaticFor<0, C::K>::run([&](auto J) {
+        const uint32_t d = dr.template bbf_draw<decltype(J)::value>(ss);
+        const uint32_t x = col[(d >> (32 - C::LGB + 5)) * 32];
+        acc &= __funnelshift_r(x, x, d >> (32 - C::LGB));
+    });
+    return acc & 1u;
+}
+
 // contains, this lane's words of a block (Θ > 1): returns the missing bits.
 template <class C>
 __device__ __forceinline__ typename C::W contains_part(const typename C::W* F, const Draws<C>& dr, uint32_t blk,
@@ -371,11 +407,11 @@ __device__ __forceinline__ void load_tile_keys(const uint64_t* keys, uint64_t mi
 // registers (kin); the keys of this warp's next full tile are loaded into
 // knext while this tile's memory accesses are in flight (software pipeline:
 // the HBM latency of the key stream hides behind a whole tile of work).
-template <class C, bool ADD, bool FULL>
+template <class C, bool ADD, bool FULL, bool USE_SM = true>
 __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_t lane, uint32_t pos,
                                          uint32_t gbase, bool vec_ok, const SaltSrc<C>& ss,
                                          const uint64_t (&kin)[C::KPT], uint64_t (&knext)[C::KPT],
-                                         bool have_next, uint64_t next_mine)
+                                         bool have_next, uint64_t next_mine, uint32_t* sm = nullptr)
 {
     using W = typename C::W;
     constexpr int KPT = C::KPT;
@@ -416,7 +452,52 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
     if constexpr (ADD || C::THETA > 1) {
         if (have_next) load_tile_keys<KPT>(p.keys, next_mine, vec_ok, knext);
     }
-    if constexpr (C::THETA == 1 && ADD) {
+    if constexpr (ADD && C::BBF_SMA && USE_SM) {
+        // (2a) every lane ORs its keys' patterns into its own columns of the
+        // warp's staging area; word q of column c lives at [q*32 + (c ^ q)]
+        // so both this phase (one column per lane) and the next (Θ lanes
+        // reading one column) spread over distinct banks
+        constexpr int NW32 = C::B / 32;
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            uint32_t* base = sm + j * NW32 * 32;
+#pragma unroll
+            for (int q = 0; q < NW32; ++q) base[q * 32 + (lane ^ q)] = 0u;
+            if (FULL || valid[j]) {
+                const Draws<C> dr(lo[j], C::HS == 1 ? lo2[j] : 0u);
+                StaticFor<0, C::K>::run([&](auto J) {
+                    const uint32_t d = dr.template bbf_draw<decltype(J)::value>(ss);
+                    const uint32_t q = d >> (32 - C::LGB + 5);
+                    atomicOr(base + q * 32 + (lane ^ q), __funnelshift_l(1u, 1u, d >> (32 - C::LGB)));
+                });
+            }
+        }
+        __syncwarp();
+        // (2b) the group's lanes take turns: lane pos issues the REDs of its
+        // words of the key owned by lane gbase + r (one L2 request per sector)
+#pragma unroll 1
+        for (int r = 0; r < C::THETA; ++r) {
+            const uint32_t src = gbase + r;
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) {
+                const uint32_t bk = __shfl_sync(0xffffffffu, blk[j], src);
+                const uint32_t* base = sm + j * NW32 * 32;
+                W* bp = (W*)p.words + (uint64_t)bk * C::s;
+                StaticFor<0, C::NSLOT>::run([&](auto SL) {
+                    const uint32_t w = C::word(decltype(SL)::value, pos);
+                    W m;
+                    if constexpr (C::S == 64) {
+                        const uint32_t q0 = 2 * w, q1 = 2 * w + 1;
+                        m = (W)base[q0 * 32 + (src ^ q0)] | ((W)base[q1 * 32 + (src ^ q1)] << 32);
+                    } else {
+                        m = base[w * 32 + (src ^ w)];
+                    }
+                    if (m) red_or(bp + w, m);  // zero for invalid keys (columns cleared)
+                });
+            }
+        }
+        __syncwarp();  // the columns are rewritten by the next tile
+    } else if constexpr (C::THETA == 1 && ADD) {
 #pragma unroll
         for (int j = 0; j < KPT; ++j)
             if (FULL || valid[j]) add_part<C>((W*)p.words, Draws<C>::make(key[j], hfull[j], p.seed), blk[j], 0, ss);
@@ -434,8 +515,14 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
         }
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
-            if (FULL || valid[j])
-                res |= (uint32_t)test_block<C>(wd[j], Draws<C>::make(key[j], hfull[j], p.seed), ss) << j;
+            if (FULL || valid[j]) {
+                if constexpr (C::BBF_SM && USE_SM)
+                    res |= (uint32_t)test_block_sm<C>(wd[j], Draws<C>::make(key[j], hfull[j], p.seed), ss,
+                                                      sm + j * (C::B / 32) * 32)
+                           << j;
+                else
+                    res |= (uint32_t)test_block<C>(wd[j], Draws<C>::make(key[j], hfull[j], p.seed), ss) << j;
+            }
         }
     } else {
         // (2) group-cooperative execution, one key of the group at a time
@@ -483,6 +570,13 @@ __global__ void __launch_bounds__(256) bulk_kernel(const Params p)
 {
     __shared__ uint32_t s_salt[C::HV == 2 ? 64 : 1];
     __shared__ uint32_t s_gsalt[C::HV == 2 ? 16 : 1];
+    constexpr bool SM = (C::BBF_SM && !ADD && C::THETA == 1) || (C::BBF_SMA && ADD);
+    __shared__ uint32_t s_bbf[SM ? C::BBF_SM_WORDS : 1];
+    // contains: this lane's column of its warp's KPT key slots; add: the
+    // warp's staging area
+    uint32_t* const sm = !SM ? nullptr
+                             : s_bbf + (threadIdx.x >> 5) * (C::KPT * (C::B / 32) * 32) +
+                                   (ADD ? 0u : (threadIdx.x & 31u));
     if constexpr (C::HV == 2) {
         if (threadIdx.x < 64) s_salt[threadIdx.x] = c_salt[threadIdx.x];
         if (threadIdx.x < 16) s_gsalt[threadIdx.x] = c_gsalt[threadIdx.x];
@@ -509,10 +603,10 @@ __global__ void __launch_bounds__(256) bulk_kernel(const Params p)
         uint64_t knext[C::KPT];
         if (t < nfull)
             run_tile<C, ADD, true>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
-                                   tn * TILE + lane * C::KPT);
+                                   tn * TILE + lane * C::KPT, sm);
         else
             run_tile<C, ADD, false>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
-                                    tn * TILE + lane * C::KPT);
+                                    tn * TILE + lane * C::KPT, sm);
         if constexpr (PF) {
 #pragma unroll
             for (int j = 0; j < C::KPT; ++j) kcur[j] = knext[j];
@@ -565,10 +659,10 @@ __global__ void __launch_bounds__(256) hybrid_add_kernel(const Params p)
             const uint64_t tn = t + nw;
             const bool have_next = tn < nfull;
             if (t < nfull)
-                run_tile<C, true, true>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
+                run_tile<C, true, true, false>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
                                         tn * TILE + lane * KPT);
             else
-                run_tile<C, true, false>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
+                run_tile<C, true, false, false>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
                                          tn * TILE + lane * KPT);
 #pragma unroll
             for (int j = 0; j < KPT; ++j) kcur[j] = knext[j];
