@@ -75,7 +75,12 @@ struct Cfg {
     // patterns into shared memory (one atomic per draw) and the group then
     // issues the coalesced REDs from there, instead of every lane of the group
     // evaluating all k draws against its own words (Θ-fold redundant work)
-    static constexpr bool BBF_SMA = (V == V_BBF) && (THETA > 1) && (B >= 256) && (BBF_SM_WORDS <= 8192);
+    // CSBF whose lanes hold whole groups (Φ a multiple of s/z): one mask and
+    // one access per group instead of a mask per word discarded unless selected
+    static constexpr bool GROUPWISE = (V == V_CSBF) && (G > 1) && (PHI % G == 0);
+    // (pays once the redundant work K*Θ is large: profiles/r1_bbf_csbf_sweep.md)
+    static constexpr bool BBF_SMA = (V == V_BBF) && (THETA > 1) && (B >= 256) && (K * THETA >= 24) &&
+                                    (BBF_SM_WORDS <= 8192);
     using W = typename WordT<S>::T;
 
     static_assert(S == 32 || S == 64, "word size");
@@ -228,6 +233,20 @@ __device__ __forceinline__ typename C::W slot_mask(const Draws<C>& dr, uint32_t 
     return m;
 }
 
+// CSBF: the mask of the group whose first word w0 is slot SL0 of this lane
+// (its Q draws, before the selector picks the word).
+template <class C, int SL0>
+__device__ __forceinline__ typename C::W group_mask(const Draws<C>& dr, uint32_t w0, const SaltSrc<C>& ss)
+{
+    using W = typename C::W;
+    W m = 0;
+    StaticFor<0, C::Q>::run([&](auto T) {
+        const uint32_t d = dr.template word_draw<SL0, decltype(T)::value>(w0, ss);
+        m |= W(1) << (d >> (32 - C::LGW));
+    });
+    return m;
+}
+
 // ----------------------------------------------------------------- per key
 // Select a[idx] from a compile-time-sized register array without local memory
 // (a SEL chain; N <= 32).
@@ -330,10 +349,19 @@ __device__ __forceinline__ typename C::W contains_part(const typename C::W* F, c
         VecLoad<C::S, C::PHI>::run(bp + decltype(ST)::value * C::THETA * C::PHI, wd + decltype(ST)::value * C::PHI);
     });
     W acc = 0;
-    StaticFor<0, C::NSLOT>::run([&](auto SL) {
-        const W m = slot_mask<C, decltype(SL)::value>(dr, C::word(decltype(SL)::value, pos), ss);
-        acc |= m & ~wd[decltype(SL)::value];
-    });
+    if constexpr (C::GROUPWISE) {
+        StaticFor<0, C::NSLOT / C::G>::run([&](auto GI) {
+            constexpr int SL0 = decltype(GI)::value * C::G;
+            const W m = group_mask<C, SL0>(dr, C::word(SL0, pos), ss);
+            const uint32_t sel = (dr.lo * ss.template gsalt<SL0>(C::word(SL0, pos))) >> (32 - C::LGG);
+            acc |= m & ~pick<C::G>(wd + SL0, sel);
+        });
+    } else {
+        StaticFor<0, C::NSLOT>::run([&](auto SL) {
+            const W m = slot_mask<C, decltype(SL)::value>(dr, C::word(decltype(SL)::value, pos), ss);
+            acc |= m & ~wd[decltype(SL)::value];
+        });
+    }
     return acc;
 }
 
@@ -344,6 +372,17 @@ __device__ __forceinline__ void add_part(typename C::W* F, const Draws<C>& dr, u
 {
     using W = typename C::W;
     W* bp = F + (uint64_t)blk * C::s;
+    if constexpr (C::GROUPWISE) {
+        // one mask and one RED per CSBF group, at the selected word
+        StaticFor<0, C::NSLOT / C::G>::run([&](auto GI) {
+            constexpr int SL0 = decltype(GI)::value * C::G;
+            const uint32_t w0 = (C::THETA == 1) ? (uint32_t)SL0 : C::word(SL0, pos);
+            const W m = group_mask<C, SL0>(dr, w0, ss);
+            const uint32_t sel = (dr.lo * ss.template gsalt<SL0>(w0)) >> (32 - C::LGG);
+            red_or(bp + w0 + sel, m);
+        });
+        return;
+    }
     StaticFor<0, C::NSLOT>::run([&](auto SL) {
         const uint32_t w = (C::THETA == 1) ? (uint32_t)decltype(SL)::value : C::word(decltype(SL)::value, pos);
         const W m = slot_mask<C, decltype(SL)::value>(dr, w, ss);

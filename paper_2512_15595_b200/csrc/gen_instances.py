@@ -34,6 +34,17 @@ def valid_k(v, B, S, z, ks):
     return out
 
 
+def default_add(v, B, S, z):
+    """The library's default add layout (bf_api.cu set_sched): Θ = s, Φ = 1
+    (P:L344), except CSBF with z < s: one lane per group (Θ = z, Φ = s/z),
+    whose group-wise masks and z REDs per key beat Θ = s by 1.2-1.9x on the
+    C2 CSBF rows (profiles/r1_csbf_groupwise.md)."""
+    s = B // S
+    if v == CSBF and z < s:
+        return z, s // z
+    return s, 1
+
+
 def layouts(s):
     out = []
     t = 1
@@ -59,6 +70,10 @@ def instances():
             add(0, v, B, S, k, z, s, 1, kpt, 0)   # add: Θ=s, Φ=1
             if s > 1:
                 add(0, v, B, S, k, z, 1, s, kpt, 0)  # add Θ=1 (BBF/CSBF may prefer it)
+            if v == CSBF and 1 < z < s:  # (z = 1 is the Θ = 1 layout above)
+                # one lane per group (Θ = z, Φ = s/z): group-wise masks (Cfg::GROUPWISE)
+                add(0, v, B, S, k, z, z, s // z, kpt, 0)
+                add(1, v, B, S, k, z, z, s // z, kpt, 0)
 
     # configs[1] sweep rows, k = 4..16 where valid
     rows = [(RBBF, 32, 32, 0), (RBBF, 64, 64, 0), (SBF, 64, 32, 0), (SBF, 128, 64, 0),
@@ -139,7 +154,7 @@ def emit():
     # binning (Θ=1 config), op 3 = phase-2 apply with the default add schedule
     binned = []
     for op, v, B, S, k, z, theta, phi, kpt, hv in inst:
-        if op == 0 and theta == B // S and phi == 1 and kpt == 4 and hv == 0:
+        if op == 0 and (theta, phi) == default_add(v, B, S, z) and kpt == 4 and hv == 0:
             binned.append((2, v, B, S, k, z, 1, 1, 1, 0))
             binned.append((3, v, B, S, k, z, theta, phi, kpt, hv))
             binned.append((4, v, B, S, k, z, 1, B // S, 1, 0))  # routed contains (Θ=1, Φ=s)

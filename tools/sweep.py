@@ -50,6 +50,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cfg", default=None, help="v,B,S,k,z for --set one")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--only-variant", type=int, default=None, help="restrict c2 to one variant id")
     a = ap.parse_args()
 
     import torch
@@ -68,7 +69,8 @@ def main():
     for op, v, B, S, k, z, th, ph, kpt, hv in inst:
         groups[(v, B, S, k, z)].append((op, th, ph, kpt, hv))
     if a.set == "c2":
-        sel = {c: s for c, s in groups.items() if 4 <= c[3] <= 16 and c[1] <= 256}
+        sel = {c: s for c, s in groups.items() if 4 <= c[3] <= 16 and c[1] <= 256
+               and (a.only_variant is None or c[0] == a.only_variant)}
         m_of = lambda c: 1 << 28  # noqa: E731
         n = a.n
     elif a.set in ("c4", "c4l2"):
