@@ -199,12 +199,17 @@ static int set_sched(bf_filter* f, int op, int theta, int phi, int kpt, int hv)
 {
     const int s = (int)f->s;
     if (theta == 0) {  // defaults
-        if (op == 0) { theta = s; phi = 1; }                       // Θ̂_a = s
-        if (op == 0 && f->variant == BF_CSBF && (int)f->z < s) {  // one lane per group (gen_instances.default_add)
-            theta = (int)f->z;
-            phi = s / (int)f->z;
+        if (op == 0) {
+            theta = s;  // Θ̂_a = s
+            phi = 1;
+            if (f->variant == BF_CSBF && (int)f->z < s) {  // one lane per group (gen_instances.default_add)
+                theta = (int)f->z;
+                phi = s / (int)f->z;
+            }
+        } else {
+            theta = f->B > 256 ? (int)f->B / 256 : 1;  // Θ̂_c = max(1, B/256)
+            phi = s / theta;
         }
-        else { theta = f->B > 256 ? (int)f->B / 256 : 1; phi = s / theta; }  // Θ̂_c = max(1, B/256)
         kpt = 4;  // 4 keys per lane: one 256-bit key load, 4 blocks in flight (profiles/r1_sweep_c2.md)
         hv = 0;
         if (f->scheme == 2) {  // iterative draws form a chain per key: one lane per key

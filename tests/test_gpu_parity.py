@@ -656,3 +656,21 @@ def test_cuda_graph_capture_and_replay(bflib, cuda):
     torch.cuda.synchronize()
     assert np.array_equal(_gpu_bytes(f), o.bytes())
     assert np.array_equal(out.cpu().numpy().view(np.uint32), o.contains(keys))
+
+
+@pytest.mark.parametrize("cfg,add_l,con_l", [
+    ((3, 256, 64, 8, 0), (4, 1, 4), (1, 4, 4)),     # SBF: add Θ=s, contains Θ=1
+    ((1, 256, 64, 8, 0), (4, 1, 4), (1, 4, 4)),     # BBF
+    ((2, 64, 64, 8, 0), (1, 1, 4), (1, 1, 4)),      # RBBF
+    ((4, 256, 32, 8, 2), (2, 4, 4), (1, 8, 4)),     # CSBF z < s: one lane per group
+    ((4, 256, 32, 8, 4), (4, 2, 4), (1, 8, 4)),
+    ((3, 1024, 64, 16, 0), (16, 1, 4), (4, 4, 4)),  # B > 256: contains Θ = B/256
+])
+def test_default_layouts(bflib, cuda, cfg, add_l, con_l):
+    """The default schedules bf_create picks, all specialized kernels."""
+    bf = bflib
+    v, B, S, k, z = cfg
+    f = bf.Filter(1 << 22, k, B, S, variant=v, z=z)
+    for op, want in ((0, add_l), (1, con_l)):
+        lay = f.layout(op)
+        assert (lay["theta"], lay["phi"], lay["kpt"], lay["specialized"]) == (*want, 1), (op, lay)
