@@ -239,6 +239,70 @@ __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
     }
 }
 
+// Phase 2, shared-memory form (filters that fit L2): the ranges are small
+// enough for shared memory (bp.lg_bpr blocks per range, <= 64 KB) and ONE CTA
+// owns a range at a time: it zeroes a shared tile, ORs every record of the
+// range's bucket into it with shared-memory atomics, and then ORs the tile
+// into the filter with one coalesced red.global.or per nonzero word.  The
+// direct kernel's bound -- the L2 atomic unit's rate for 32-byte RED sectors
+// (R_red) -- is gone: global atomics drop from s per key to s*b per batch.
+// The write-back is an OR, not a store, so adds running concurrently on
+// other streams are never lost.  C1 is the filter's Θ=1 configuration.
+constexpr int SMA_THREADS = 512;
+
+template <class C1>
+__global__ void __launch_bounds__(SMA_THREADS) apply_smem_kernel(const BinParams bp)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    using W = typename C1::W;
+    constexpr int s = C1::s;
+    W* tile = (W*)smem;
+    SaltSrc<C1> ss;
+    ss.init(0, nullptr, nullptr);
+    const uint32_t tid = threadIdx.x;
+    const uint64_t bpr = 1ULL << bp.lg_bpr;
+    const uint32_t wpr = (uint32_t)(bpr * s);
+    W* F = (W*)bp.f.words;
+    const uint64_t total_words = bp.f.b * s;
+    for (uint32_t r = blockIdx.x; r < bp.nranges; r += gridDim.x) {
+        const uint64_t w0 = (uint64_t)r * wpr;
+        const uint32_t nw = (uint32_t)min((uint64_t)wpr, total_words - w0);
+        for (uint32_t i = tid; i < wpr; i += SMA_THREADS) tile[i] = W(0);
+        __syncthreads();
+        const uint64_t cnt = min((uint64_t)bp.cursor[r], bp.cap);
+        const uint64_t* rp = bp.recs + (uint64_t)r * bp.cap;
+        const uint32_t blk0 = (uint32_t)(r * bpr);
+        constexpr int RPT = 4;  // records per thread per step: one 256-bit load
+        const uint64_t nfull = cnt / (SMA_THREADS * RPT);
+        for (uint64_t it = 0; it <= nfull; ++it) {
+            const uint64_t i0 = it * (SMA_THREADS * RPT) + (uint64_t)tid * RPT;
+            uint64_t rec[RPT];
+            if (it < nfull) {
+                ld_keys4(rp + i0, rec);
+            } else {
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) rec[j] = i0 + j < cnt ? ld_key1(rp + i0 + j) : ~0ULL;
+            }
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                if (rec[j] == ~0ULL) continue;  // (block 2^32-1 with lo 2^32-1 never occurs past the tail)
+                const Draws<C1> dr((uint32_t)rec[j]);
+                W* bw = tile + ((uint32_t)(rec[j] >> 32) - blk0) * s;
+                StaticFor<0, s>::run([&](auto SL) {
+                    const W m = slot_mask<C1, decltype(SL)::value>(dr, (uint32_t)decltype(SL)::value, ss);
+                    if (m) atomicOr(bw + decltype(SL)::value, m);
+                });
+            }
+        }
+        __syncthreads();
+        for (uint32_t i = tid; i < nw; i += SMA_THREADS) {
+            const W v = tile[i];
+            if (v) red_or(F + w0 + i, v);
+        }
+        __syncthreads();
+    }
+}
+
 // Routed lookup (NEXT N1): test the records of every source bucket against
 // the local part of the filter; one result byte per record slot.  C is a
 // Θ=1 contains configuration.

@@ -70,22 +70,70 @@ static __constant__ uint32_t c_gsalt[16] = {
 // ---------------------------------------------------------------- hashing
 __device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
 
+// (hi:lo) *= C mod 2^64 in three IMADs: one IMAD.WIDE for lo*C_lo, then the
+// two cross products accumulate into the high word (left to itself, ptxas
+// expands a 64-bit multiply into four, splitting the chain for latency).
+template <uint64_t C>
+__device__ __forceinline__ void mul64c(uint32_t& lo, uint32_t& hi)
+{
+    constexpr uint32_t cl = (uint32_t)C, ch = (uint32_t)(C >> 32);
+    uint32_t l, h;
+    asm("{\n\t.reg .b64 w;\n\t"
+        "mul.wide.u32 w, %2, %4;\n\t"
+        "mov.b64 {%0, %1}, w;\n\t"
+        "mad.lo.u32 %1, %3, %4, %1;\n\t"
+        "mad.lo.u32 %1, %2, %5, %1;\n\t}"
+        : "=&r"(l), "=&r"(h)
+        : "r"(lo), "r"(hi), "n"(cl), "n"(ch));
+    lo = l;
+    hi = h;
+}
+
+// 64-bit rotate left by R < 32 on (hi:lo): two funnel shifts.
+template <int R>
+__device__ __forceinline__ void rotl64c(uint32_t& lo, uint32_t& hi)
+{
+    const uint32_t l = __funnelshift_l(hi, lo, R), h = __funnelshift_l(lo, hi, R);
+    lo = l;
+    hi = h;
+}
+
 // XXH64 of the 8 little-endian bytes of `key` (the xxHash 8-byte path; the GPU
-// is little-endian so the register value is the LE byte string).
+// is little-endian so the register value is the LE byte string), on 32-bit
+// halves: 5 multiplies x 3 IMAD, 2 rotates x 2 SHF, and the xor-shifts
+// touch only the half they change (h ^= h >> 33 is lo ^= hi >> 1).
+//   h = seed + P5 + 8;  h ^= rotl(key * P2, 31) * P1
+//   h = rotl(h, 27) * P1 + P4
+//   h ^= h >> 33;  h *= P2;  h ^= h >> 29;  h *= P3;  h ^= h >> 32
 __device__ __forceinline__ uint64_t xxh64_u64(uint64_t key, uint64_t seed)
 {
-    uint64_t h = seed + XXP5 + 8ULL;
-    uint64_t k1 = key * XXP2;
-    k1 = rotl64(k1, 31);
-    k1 *= XXP1;
-    h ^= k1;
-    h = rotl64(h, 27) * XXP1 + XXP4;
-    h ^= h >> 33;
-    h *= XXP2;
-    h ^= h >> 29;
-    h *= XXP3;
-    h ^= h >> 32;
-    return h;
+#ifdef BF_DIAG_NOHASH  // diagnostic only (tools/kexp): keys are already uniform
+    return key ^ seed;
+#endif
+    const uint64_t h0 = seed + XXP5 + 8ULL;
+    uint32_t lo = (uint32_t)key, hi = (uint32_t)(key >> 32);
+    mul64c<XXP2>(lo, hi);
+    rotl64c<31>(lo, hi);
+    mul64c<XXP1>(lo, hi);
+    lo ^= (uint32_t)h0;
+    hi ^= (uint32_t)(h0 >> 32);
+    rotl64c<27>(lo, hi);
+    mul64c<XXP1>(lo, hi);
+    {  // + P4 (64-bit add with carry)
+        uint32_t l, h;
+        asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;"
+            : "=r"(l), "=r"(h)
+            : "r"(lo), "r"(hi), "n"((uint32_t)XXP4), "n"((uint32_t)(XXP4 >> 32)));
+        lo = l;
+        hi = h;
+    }
+    lo ^= hi >> 1;  // h ^= h >> 33
+    mul64c<XXP2>(lo, hi);
+    lo ^= __funnelshift_r(lo, hi, 29);  // h ^= h >> 29
+    hi ^= hi >> 29;
+    mul64c<XXP3>(lo, hi);
+    lo ^= hi;  // h ^= h >> 32
+    return ((uint64_t)hi << 32) | lo;
 }
 
 // SplitMix64 output function (synthetic key generator).
@@ -131,6 +179,11 @@ __device__ __forceinline__ unsigned long long shl_clamp(unsigned long long v, ui
 // marks them evict-first in L2; ptxas accepts .L2::evict_first only there).
 __device__ __forceinline__ void ld_keys4(const uint64_t* p, uint64_t (&k)[4])
 {
+#ifdef BF_KEY_L1
+    asm("ld.global.nc.L1::evict_first.L2::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(k[0]), "=l"(k[1]), "=l"(k[2]), "=l"(k[3]) : "l"(p));
+    return;
+#endif
     asm("ld.global.nc.L1::no_allocate.L2::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
                  : "=l"(k[0]), "=l"(k[1]), "=l"(k[2]), "=l"(k[3]) : "l"(p));
 }

@@ -33,6 +33,20 @@
 
 #include "bf_device.cuh"
 
+// Experiment knobs (tools/kexp): compile-time overrides of schedule rules.
+#ifndef BF_T1_PF_MODE
+#define BF_T1_PF_MODE 0  // Θ=1 contains key prefetch into registers: 0 rule, 1 always, 2 never
+#endif
+#ifndef BF_L2PF_DIST
+#define BF_L2PF_DIST -1  // contains: prefetch keys this many tiles ahead into L2 (0 off, -1 rule)
+#endif
+#ifndef BF_T1_PIPE
+#define BF_T1_PIPE 0  // Θ=1 contains: two half-tiles of block loads in flight (software pipeline)
+#endif
+#ifndef BF_L1PF_DIST
+#define BF_L1PF_DIST 0  // contains: prefetch the key tile this many tiles ahead into L1 (0: off)
+#endif
+
 namespace bf {
 
 struct Params {
@@ -64,13 +78,20 @@ struct Cfg {
     // Θ=1 contains loads the next tile's keys while this tile's blocks are in
     // flight only when the KPT loaded blocks leave room for them
     // (KPT*s*S/32 registers); add and cooperative contains always do
-    static constexpr bool PREFETCH_T1 = (KPT * s * S / 32 <= 16);
+    static constexpr bool PREFETCH_T1 =
+        BF_T1_PF_MODE == 1 ? true : (BF_T1_PF_MODE == 2 ? false : (KPT * s * S / 32 <= 16));
     // BBF contains (Θ = 1) with B >= 256 tests its draws against a copy of
     // the block in shared memory instead of selecting the word among s
     // registers (a SEL chain of s-1 steps per draw): per-CTA staging of
     // 8 warps x KPT keys x B/32 words x 32 lanes, <= 32 KB
     static constexpr int BBF_SM_WORDS = 8 * KPT * (B / 32) * 32;
     static constexpr bool BBF_SM = (V == V_BBF) && (B >= 256) && (BBF_SM_WORDS <= 8192);
+    // Θ=1 contains without the register key prefetch (PREFETCH_T1) touches the key tile two
+    // grid strides ahead with prefetch.global.L2 (one request per 128-byte
+    // line, no registers): the key load at the top of a tile then waits for
+    // L2 instead of HBM (+4-7% on SBF 256/64, kexp; no gain where keys are
+    // already register-prefetched or the block is staged in shared memory)
+    static constexpr int L2PF = BF_L2PF_DIST >= 0 ? BF_L2PF_DIST : ((THETA == 1 && !PREFETCH_T1 && !BBF_SM) ? 2 : 0);
     // BBF add (Θ > 1) with B >= 256: each lane ORs its own keys' whole
     // patterns into shared memory (one atomic per draw) and the group then
     // issues the coalesced REDs from there, instead of every lane of the group
@@ -395,6 +416,11 @@ __device__ __forceinline__ void add_part(typename C::W* F, const Draws<C>& dr, u
 }
 
 // ----------------------------------------------------------------- results
+// Bit i of word w of the output is key 32w + i (LSB-first).  A tile's key
+// slot j of lane l is key l*KPT + j of the tile, so output word q of the tile
+// is the OR over the 32/KPT lanes l of group q of res_l << (KPT*(l mod
+// 32/KPT)): shift, log2(32/KPT) shuffle-xor steps, and the first lane of each
+// group stores its word (KPT lanes store KPT consecutive words).
 template <int KPT>
 __device__ __forceinline__ void store_results(uint32_t* out, uint64_t tile, uint32_t res, uint32_t lane,
                                               uint64_t nwords)
@@ -402,26 +428,13 @@ __device__ __forceinline__ void store_results(uint32_t* out, uint64_t tile, uint
     if constexpr (KPT == 1) {
         const uint32_t b = __ballot_sync(0xffffffffu, res & 1u);
         if (lane == 0 && tile < nwords) out[tile] = b;
-    } else if constexpr (KPT == 2) {
-        const uint32_t b0 = __ballot_sync(0xffffffffu, res & 1u);
-        const uint32_t b1 = __ballot_sync(0xffffffffu, (res >> 1) & 1u);
-        if (lane < 2) {
-            const uint64_t idx = tile * 2 + lane;
-            const uint32_t wv = spread2(b0 >> (16 * lane)) | (spread2(b1 >> (16 * lane)) << 1);
-            if (idx < nwords) out[idx] = wv;
-        }
     } else {
-        const uint32_t b0 = __ballot_sync(0xffffffffu, res & 1u);
-        const uint32_t b1 = __ballot_sync(0xffffffffu, (res >> 1) & 1u);
-        const uint32_t b2 = __ballot_sync(0xffffffffu, (res >> 2) & 1u);
-        const uint32_t b3 = __ballot_sync(0xffffffffu, (res >> 3) & 1u);
-        if (lane < 4) {
-            const uint64_t idx = tile * 4 + lane;
-            const uint32_t sh = 8 * lane;
-            const uint32_t wv = spread4(b0 >> sh) | (spread4(b1 >> sh) << 1) | (spread4(b2 >> sh) << 2) |
-                                (spread4(b3 >> sh) << 3);
-            if (idx < nwords) out[idx] = wv;
-        }
+        constexpr uint32_t LPW = 32 / KPT;  // lanes per output word
+        uint32_t v = res << (KPT * (lane & (LPW - 1)));
+#pragma unroll
+        for (uint32_t d = 1; d < LPW; d <<= 1) v |= __shfl_xor_sync(0xffffffffu, v, d);
+        const uint64_t idx = tile * KPT + lane / LPW;
+        if ((lane & (LPW - 1)) == 0 && idx < nwords) out[idx] = v;
     }
 }
 
@@ -432,6 +445,10 @@ template <int KPT>
 __device__ __forceinline__ void load_tile_keys(const uint64_t* keys, uint64_t mine, bool vec_ok,
                                                uint64_t (&key)[KPT])
 {
+#ifdef BF_DIAG_SYNTHKEYS  // diagnostic only (tools/kexp): keys made in registers, no key stream
+    for (int j = 0; j < KPT; ++j) key[j] = mix64(mine + j);
+    return;
+#endif
     if (vec_ok) {
         if constexpr (KPT == 4) ld_keys4(keys + mine, key);
         else if constexpr (KPT == 2) ld_keys2(keys + mine, key);
@@ -604,6 +621,88 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
     if constexpr (!ADD) store_results<KPT>(p.out, tile, res, lane, (p.n + 31) / 32);
 }
 
+// Θ = 1 contains, software-pipelined over half tiles.  A lane's KPT keys
+// of a tile are split into halves A (keys 0..H-1) and B (H..KPT-1); the loads
+// of one half are always in flight while the other half is tested:
+//   issue B(t) | load keys(t+1) | test A(t) | issue A(t+1) | test B(t) | store
+// so a warp never waits with nothing in flight (the plain tile loop issues
+// all KPT loads, then idles until they return).  Full tiles only; the ragged
+// tail goes through run_tile.  Same bits as every other schedule.
+template <class C>
+__device__ __forceinline__ void contains_pipe(const Params& p, uint32_t* sm)
+{
+    using W = typename C::W;
+    constexpr int KPT = C::KPT, H = KPT / 2;
+    static_assert(C::THETA == 1 && KPT >= 2 && C::HS == 0, "pipelined contains: Θ = 1, KPT >= 2, multiplicative draws");
+    const uint32_t lane = threadIdx.x & 31u;
+    SaltSrc<C> ss;
+    ss.init(0, nullptr, nullptr);
+    constexpr uint64_t TILE = 32 * KPT;
+    const uint64_t ntiles = (p.n + TILE - 1) / TILE;
+    const uint64_t nfull = p.n / TILE;
+    const uint64_t nwords = (p.n + 31) / 32;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const bool vec_ok = (((uintptr_t)p.keys) & (8 * KPT - 1)) == 0;
+    const W* F = (const W*)p.words;
+    auto test = [&](const W* wd, uint32_t lo, int slot) -> uint32_t {
+        const Draws<C> dr(lo);
+        if constexpr (C::BBF_SM) return (uint32_t)test_block_sm<C>(wd, dr, ss, sm + slot * (C::B / 32) * 32);
+        else return (uint32_t)test_block<C>(wd, dr, ss);
+    };
+    if (gw < nfull) {
+        uint64_t kc[KPT];
+        load_tile_keys<KPT>(p.keys, gw * TILE + lane * KPT, vec_ok, kc);
+        uint32_t loA[H], loB[H];
+        W wa[H][C::s], wb[H][C::s];
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+            const uint64_t h = xxh64_u64(kc[j], p.seed);
+            loA[j] = (uint32_t)h;
+            load_block<C>(F, block_of(h, p.b32), wa[j]);
+        }
+        for (uint64_t t = gw; t < nfull; t += nw) {
+            const uint64_t tn = t + nw;
+            const bool have_next = tn < nfull;
+#pragma unroll
+            for (int j = 0; j < H; ++j) {
+                const uint64_t h = xxh64_u64(kc[H + j], p.seed);
+                loB[j] = (uint32_t)h;
+                load_block<C>(F, block_of(h, p.b32), wb[j]);
+            }
+            uint64_t kn[KPT];
+            if (have_next) load_tile_keys<KPT>(p.keys, tn * TILE + lane * KPT, vec_ok, kn);
+            if constexpr (C::L2PF > 0) {
+                const uint64_t tp = t + (uint64_t)C::L2PF * nw;
+                if (tp < nfull && (lane & 3u) == 0)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.keys + tp * TILE + lane * KPT));
+            }
+            uint32_t res = 0;
+#pragma unroll
+            for (int j = 0; j < H; ++j) res |= test(wa[j], loA[j], j) << j;
+            if (have_next) {
+#pragma unroll
+                for (int j = 0; j < H; ++j) {
+                    const uint64_t h = xxh64_u64(kn[j], p.seed);
+                    loA[j] = (uint32_t)h;
+                    load_block<C>(F, block_of(h, p.b32), wa[j]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < H; ++j) res |= test(wb[j], loB[j], H + j) << (H + j);
+            store_results<KPT>(p.out, t, res, lane, nwords);
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) kc[j] = kn[j];
+        }
+    }
+    // ragged tail: at most one partial tile, taken by the warp the grid
+    // stride would give it
+    if (ntiles > nfull && gw == nfull % nw) {
+        uint64_t kin[KPT] = {}, knext[KPT];
+        run_tile<C, false, false>(p, nfull, lane, 0, 0, vec_ok, ss, kin, knext, false, 0, sm);
+    }
+}
+
 template <class C, bool ADD>
 __global__ void __launch_bounds__(256) bulk_kernel(const Params p)
 {
@@ -620,6 +719,10 @@ __global__ void __launch_bounds__(256) bulk_kernel(const Params p)
         if (threadIdx.x < 64) s_salt[threadIdx.x] = c_salt[threadIdx.x];
         if (threadIdx.x < 16) s_gsalt[threadIdx.x] = c_gsalt[threadIdx.x];
         __syncthreads();
+    }
+    if constexpr (!ADD && BF_T1_PIPE && C::THETA == 1 && C::KPT >= 2 && C::HS == 0 && C::HV == 0) {
+        contains_pipe<C>(p, sm);
+        return;
     }
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t pos = lane & (uint32_t)(C::THETA - 1);
@@ -640,6 +743,16 @@ __global__ void __launch_bounds__(256) bulk_kernel(const Params p)
         const uint64_t tn = t + nw;
         const bool have_next = tn < nfull;
         uint64_t knext[C::KPT];
+        if constexpr (C::L2PF > 0 && !ADD) {
+            const uint64_t tp = t + (uint64_t)C::L2PF * nw;
+            if (tp < nfull && (lane & 3u) == 0)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p.keys + tp * TILE + lane * C::KPT));
+        }
+        if constexpr (BF_L1PF_DIST > 0 && !ADD) {
+            const uint64_t tp = t + (uint64_t)BF_L1PF_DIST * nw;
+            if (tp < nfull && (lane & 3u) == 0)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(p.keys + tp * TILE + lane * C::KPT));
+        }
         if (t < nfull)
             run_tile<C, ADD, true>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
                                    tn * TILE + lane * C::KPT, sm);

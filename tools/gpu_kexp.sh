@@ -1,0 +1,7 @@
+# Run every built experiment binary (tools/kexp/kexp_*) on the GPU.
+mkdir -p gpurun_out
+TAG=${TAG:-kx}
+for b in tools/kexp/kexp_*; do
+  echo "== $(basename $b)" >> gpurun_out/kexp_$TAG.log
+  timeout 300 $b >> gpurun_out/kexp_$TAG.log 2>&1
+done
