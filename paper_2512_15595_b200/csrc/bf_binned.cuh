@@ -49,9 +49,9 @@ constexpr int BIN_KPT = 8;
 constexpr int BIN_CHUNK = BIN_THREADS * BIN_KPT;  // keys per CTA chunk
 
 // dynamic smem layout: stage[CHUNK] u64 | hist[R] u32 (+pad) | gbase[R] u64 | stage_r[CHUNK] u16 | stage_li[CHUNK] u16
-__host__ __device__ inline size_t bin_smem_bytes(uint32_t nranges)
+__host__ __device__ inline size_t bin_smem_bytes(uint32_t nranges, uint32_t chunk = BIN_CHUNK)
 {
-    return (size_t)BIN_CHUNK * 8 + (size_t)(nranges + 1) * 4 + (size_t)nranges * 8 + (size_t)BIN_CHUNK * 4;
+    return (size_t)chunk * 8 + (size_t)(nranges + 1) * 4 + (size_t)nranges * 8 + (size_t)chunk * 4;
 }
 
 // owner of a block under the partition bounds (bounds[0] = 0, bounds[P] = b)
@@ -107,17 +107,18 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t* a, uint32_t n
 }
 
 // Phase 1.  C1 is the Θ=1 configuration of the filter (for the overflow path).
-template <class C1>
-__global__ void __launch_bounds__(BIN_THREADS) bin_kernel(const BinParams bp)
+template <class C1, int NT = BIN_THREADS, int KPT = BIN_KPT>
+__global__ void __launch_bounds__(NT) bin_kernel(const BinParams bp)
 {
+    constexpr int CHUNK = NT * KPT;
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t R = bp.nranges;
     uint64_t* stage = (uint64_t*)smem;
-    uint32_t* hist = (uint32_t*)(stage + BIN_CHUNK);
+    uint32_t* hist = (uint32_t*)(stage + CHUNK);
     unsigned long long* gbase = (unsigned long long*)(hist + R + (R & 1));
     uint16_t* stage_r = (uint16_t*)(gbase + R);
-    uint16_t* stage_li = stage_r + BIN_CHUNK;
-    __shared__ uint32_t warp_tot[BIN_THREADS / 32 + 1];
+    uint16_t* stage_li = stage_r + CHUNK;
+    __shared__ uint32_t warp_tot[NT / 32 + 1];
 
     using W = typename C1::W;
     SaltSrc<C1> ss;
@@ -125,17 +126,17 @@ __global__ void __launch_bounds__(BIN_THREADS) bin_kernel(const BinParams bp)
     const Params& p = bp.f;
     const uint32_t tid = threadIdx.x;
 
-    for (uint64_t c = blockIdx.x; c * BIN_CHUNK < p.n; c += gridDim.x) {
-        const uint64_t base = c * BIN_CHUNK;
-        const uint32_t cnt = (uint32_t)min((uint64_t)BIN_CHUNK, p.n - base);
-        for (uint32_t r = tid; r < R; r += BIN_THREADS) hist[r] = 0;
+    for (uint64_t c = blockIdx.x; c * CHUNK < p.n; c += gridDim.x) {
+        const uint64_t base = c * CHUNK;
+        const uint32_t cnt = (uint32_t)min((uint64_t)CHUNK, p.n - base);
+        for (uint32_t r = tid; r < R; r += NT) hist[r] = 0;
         __syncthreads();
         // hash once per key; count per range (coalesced key loads: i*256+tid)
-        uint64_t rec[BIN_KPT];
-        uint32_t rl[BIN_KPT];
+        uint64_t rec[KPT];
+        uint32_t rl[KPT];
 #pragma unroll
-        for (int i = 0; i < BIN_KPT; ++i) {
-            const uint32_t li = i * BIN_THREADS + tid;
+        for (int i = 0; i < KPT; ++i) {
+            const uint32_t li = i * NT + tid;
             rl[i] = 0xFFFFFFFFu;
             if (li < cnt) {
                 const uint64_t h = xxh64_u64(ld_key1(p.keys + base + li), p.seed);
@@ -147,22 +148,22 @@ __global__ void __launch_bounds__(BIN_THREADS) bin_kernel(const BinParams bp)
         }
         __syncthreads();
         // reserve this chunk's run in every touched bucket
-        for (uint32_t r = tid; r < R; r += BIN_THREADS)
+        for (uint32_t r = tid; r < R; r += NT)
             gbase[r] = hist[r] ? atomicAdd(&bp.cursor[r], (unsigned long long)hist[r]) : 0ULL;
-        block_exclusive_scan<BIN_THREADS>(hist, R, warp_tot);  // hist -> run offsets in stage
+        block_exclusive_scan<NT>(hist, R, warp_tot);  // hist -> run offsets in stage
         // counting-sort the records by range in shared memory
 #pragma unroll
-        for (int i = 0; i < BIN_KPT; ++i) {
+        for (int i = 0; i < KPT; ++i) {
             if (rl[i] != 0xFFFFFFFFu) {
                 const uint32_t r = rl[i] >> 16, pos = hist[r] + (rl[i] & 0xFFFFu);
                 stage[pos] = rec[i];
                 stage_r[pos] = (uint16_t)r;
-                stage_li[pos] = (uint16_t)(i * BIN_THREADS + tid);
+                stage_li[pos] = (uint16_t)(i * NT + tid);
             }
         }
         __syncthreads();
         // write the runs out (consecutive slots of a run -> consecutive addresses)
-        for (uint32_t j = tid; j < cnt; j += BIN_THREADS) {
+        for (uint32_t j = tid; j < cnt; j += NT) {
             const uint32_t r = stage_r[j];
             const unsigned long long off = gbase[r] + (j - hist[r]);
             const uint64_t v = stage[j];
@@ -236,70 +237,6 @@ __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
                 }
             }
         }
-    }
-}
-
-// Phase 2, shared-memory form (filters that fit L2): the ranges are small
-// enough for shared memory (bp.lg_bpr blocks per range, <= 64 KB) and ONE CTA
-// owns a range at a time: it zeroes a shared tile, ORs every record of the
-// range's bucket into it with shared-memory atomics, and then ORs the tile
-// into the filter with one coalesced red.global.or per nonzero word.  The
-// direct kernel's bound -- the L2 atomic unit's rate for 32-byte RED sectors
-// (R_red) -- is gone: global atomics drop from s per key to s*b per batch.
-// The write-back is an OR, not a store, so adds running concurrently on
-// other streams are never lost.  C1 is the filter's Θ=1 configuration.
-constexpr int SMA_THREADS = 512;
-
-template <class C1>
-__global__ void __launch_bounds__(SMA_THREADS) apply_smem_kernel(const BinParams bp)
-{
-    extern __shared__ __align__(16) unsigned char smem[];
-    using W = typename C1::W;
-    constexpr int s = C1::s;
-    W* tile = (W*)smem;
-    SaltSrc<C1> ss;
-    ss.init(0, nullptr, nullptr);
-    const uint32_t tid = threadIdx.x;
-    const uint64_t bpr = 1ULL << bp.lg_bpr;
-    const uint32_t wpr = (uint32_t)(bpr * s);
-    W* F = (W*)bp.f.words;
-    const uint64_t total_words = bp.f.b * s;
-    for (uint32_t r = blockIdx.x; r < bp.nranges; r += gridDim.x) {
-        const uint64_t w0 = (uint64_t)r * wpr;
-        const uint32_t nw = (uint32_t)min((uint64_t)wpr, total_words - w0);
-        for (uint32_t i = tid; i < wpr; i += SMA_THREADS) tile[i] = W(0);
-        __syncthreads();
-        const uint64_t cnt = min((uint64_t)bp.cursor[r], bp.cap);
-        const uint64_t* rp = bp.recs + (uint64_t)r * bp.cap;
-        const uint32_t blk0 = (uint32_t)(r * bpr);
-        constexpr int RPT = 4;  // records per thread per step: one 256-bit load
-        const uint64_t nfull = cnt / (SMA_THREADS * RPT);
-        for (uint64_t it = 0; it <= nfull; ++it) {
-            const uint64_t i0 = it * (SMA_THREADS * RPT) + (uint64_t)tid * RPT;
-            uint64_t rec[RPT];
-            if (it < nfull) {
-                ld_keys4(rp + i0, rec);
-            } else {
-#pragma unroll
-                for (int j = 0; j < RPT; ++j) rec[j] = i0 + j < cnt ? ld_key1(rp + i0 + j) : ~0ULL;
-            }
-#pragma unroll
-            for (int j = 0; j < RPT; ++j) {
-                if (rec[j] == ~0ULL) continue;  // (block 2^32-1 with lo 2^32-1 never occurs past the tail)
-                const Draws<C1> dr((uint32_t)rec[j]);
-                W* bw = tile + ((uint32_t)(rec[j] >> 32) - blk0) * s;
-                StaticFor<0, s>::run([&](auto SL) {
-                    const W m = slot_mask<C1, decltype(SL)::value>(dr, (uint32_t)decltype(SL)::value, ss);
-                    if (m) atomicOr(bw + decltype(SL)::value, m);
-                });
-            }
-        }
-        __syncthreads();
-        for (uint32_t i = tid; i < nw; i += SMA_THREADS) {
-            const W v = tile[i];
-            if (v) red_or(F + w0 + i, v);
-        }
-        __syncthreads();
     }
 }
 

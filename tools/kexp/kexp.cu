@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "bf_kernels.cuh"
+#include "bf_binned.cuh"
 
 using namespace bf;
 
@@ -101,6 +102,153 @@ static void run(Ctx& c, const char* name)
     fflush(stdout);
 }
 
+namespace bf {
+// EXPERIMENT (rejected): phase 2 in shared memory for filters that fit L2: the ranges are small
+// enough for shared memory (bp.lg_bpr blocks per range, <= 64 KB) and ONE CTA
+// owns a range at a time: it zeroes a shared tile, ORs every record of the
+// range's bucket into it with shared-memory atomics, and then ORs the tile
+// into the filter with one coalesced red.global.or per nonzero word.  The
+// direct kernel's bound -- the L2 atomic unit's rate for 32-byte RED sectors
+// (R_red) -- is gone: global atomics drop from s per key to s*b per batch.
+// The write-back is an OR, not a store, so adds running concurrently on
+// other streams are never lost.  C1 is the filter's Θ=1 configuration.
+constexpr int SMA_THREADS = 512;
+
+template <class C1>
+__global__ void __launch_bounds__(SMA_THREADS) apply_smem_kernel(const BinParams bp)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    using W = typename C1::W;
+    constexpr int s = C1::s;
+    W* tile = (W*)smem;
+    SaltSrc<C1> ss;
+    ss.init(0, nullptr, nullptr);
+    const uint32_t tid = threadIdx.x;
+    const uint64_t bpr = 1ULL << bp.lg_bpr;
+    const uint32_t wpr = (uint32_t)(bpr * s);
+    W* F = (W*)bp.f.words;
+    const uint64_t total_words = bp.f.b * s;
+    for (uint32_t r = blockIdx.x; r < bp.nranges; r += gridDim.x) {
+        const uint64_t w0 = (uint64_t)r * wpr;
+        const uint32_t nw = (uint32_t)min((uint64_t)wpr, total_words - w0);
+        for (uint32_t i = tid; i < wpr; i += SMA_THREADS) tile[i] = W(0);
+        __syncthreads();
+        const uint64_t cnt = min((uint64_t)bp.cursor[r], bp.cap);
+        const uint64_t* rp = bp.recs + (uint64_t)r * bp.cap;
+        const uint32_t blk0 = (uint32_t)(r * bpr);
+        constexpr int RPT = 4;  // records per thread per step: one 256-bit load
+        const uint64_t nfull = cnt / (SMA_THREADS * RPT);
+        for (uint64_t it = 0; it <= nfull; ++it) {
+            const uint64_t i0 = it * (SMA_THREADS * RPT) + (uint64_t)tid * RPT;
+            uint64_t rec[RPT];
+            if (it < nfull) {
+                ld_keys4(rp + i0, rec);
+            } else {
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) rec[j] = i0 + j < cnt ? ld_key1(rp + i0 + j) : ~0ULL;
+            }
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                if (rec[j] == ~0ULL) continue;  // (block 2^32-1 with lo 2^32-1 never occurs past the tail)
+                const Draws<C1> dr((uint32_t)rec[j]);
+                W* bw = tile + ((uint32_t)(rec[j] >> 32) - blk0) * s;
+                StaticFor<0, s>::run([&](auto SL) {
+                    const W m = slot_mask<C1, decltype(SL)::value>(dr, (uint32_t)decltype(SL)::value, ss);
+                    if constexpr (C1::S == 64) {  // 32-bit ATOMS.OR halves (64-bit is a CAS loop)
+                        uint32_t* h = (uint32_t*)(bw + decltype(SL)::value);
+                        if ((uint32_t)m) atomicOr(h, (uint32_t)m);
+                        if ((uint32_t)(m >> 32)) atomicOr(h + 1, (uint32_t)(m >> 32));
+                    } else {
+                        if (m) atomicOr(bw + decltype(SL)::value, m);
+                    }
+                });
+            }
+        }
+        __syncthreads();
+        for (uint32_t i = tid; i < nw; i += SMA_THREADS) {
+            const W v = tile[i];
+            if (v) red_or(F + w0 + i, v);
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace bf
+
+// binned add with the shared-memory apply (bf_binned.cuh): bin + apply_smem,
+// timed together; the filter must equal the direct add's.
+template <class C1, int NT = BIN_THREADS, int BK = BIN_KPT>
+static void run_binned(Ctx& c, const char* name, uint32_t range_kb, const char* want_hash)
+{
+    const uint64_t B = C1::B;
+    const uint64_t b = c.m_bits / B;
+    uint32_t lg = 0;
+    while ((B / 8) << (lg + 1) <= (uint64_t)range_kb * 1024) ++lg;
+    const uint32_t R = (uint32_t)((b + (1ULL << lg) - 1) >> lg);
+    const uint64_t cap = ((c.n / R + c.n / R / 32 + 8192) + 127) & ~127ULL;
+    static uint64_t* recs = nullptr;
+    static unsigned long long* cursor = nullptr;
+    static size_t recs_bytes = 0;
+    if (recs_bytes < R * cap * 8) {
+        if (recs) cudaFree(recs);
+        CK(cudaMalloc(&recs, R * cap * 8));
+        recs_bytes = R * cap * 8;
+    }
+    if (!cursor) CK(cudaMalloc(&cursor, 65536 * 8));
+    BinParams bp{};
+    bp.f.words = c.words;
+    bp.f.b = b;
+    bp.f.b32 = (uint32_t)b;
+    bp.f.keys = c.keys;
+    bp.f.n = c.n;
+    bp.recs = recs;
+    bp.cursor = cursor;
+    bp.cap = cap;
+    bp.lg_bpr = lg;
+    bp.nranges = R;
+    const size_t sm_bin = bin_smem_bytes(R, NT * BK);
+    CK(cudaFuncSetAttribute(bin_kernel<C1, NT, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bin));
+    const size_t sm_app = (size_t)(1u << lg) * (B / 8);
+    CK(cudaFuncSetAttribute(apply_smem_kernel<C1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_app));
+    int nsm = 0, occ_bin = 0, occ_app = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_bin, bin_kernel<C1, NT, BK>, NT, sm_bin));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_app, apply_smem_kernel<C1>, SMA_THREADS, sm_app));
+    const uint64_t chunks = (c.n + NT * BK - 1) / (NT * BK);
+    const int gb = (int)std::min<uint64_t>(chunks, (uint64_t)occ_bin * nsm);
+    const int ga = (int)std::min<uint64_t>(R, (uint64_t)occ_app * nsm);
+    CK(cudaMemset(c.words, 0, c.m_bits / 8));
+    std::vector<float> tb, ta, tt;
+    cudaEvent_t em;
+    CK(cudaEventCreate(&em));
+    for (int r = 0; r < c.reps + 2; ++r) {
+        CK(cudaEventRecord(c.e0));
+        CK(cudaMemsetAsync(cursor, 0, R * 8));
+        bin_kernel<C1, NT, BK><<<gb, NT, sm_bin>>>(bp);
+        CK(cudaEventRecord(em));
+        apply_smem_kernel<C1><<<ga, SMA_THREADS, sm_app>>>(bp);
+        CK(cudaEventRecord(c.e1));
+        CK(cudaEventSynchronize(c.e1));
+        CK(cudaGetLastError());
+        float a, bb;
+        CK(cudaEventElapsedTime(&a, c.e0, em));
+        CK(cudaEventElapsedTime(&bb, em, c.e1));
+        if (r >= 2) { tb.push_back(a); ta.push_back(bb); tt.push_back(a + bb); }
+    }
+    std::sort(tb.begin(), tb.end());
+    std::sort(ta.begin(), ta.end());
+    std::sort(tt.begin(), tt.end());
+    std::vector<unsigned char> fb(c.m_bits / 8);
+    CK(cudaMemcpy(fb.data(), c.words, fb.size(), cudaMemcpyDeviceToHost));
+    char hs[32];
+    snprintf(hs, sizeof hs, "%016llx", (unsigned long long)fnv(fb.data(), fb.size()));
+    printf("{\"cfg\": \"%s\", \"nt\": %d, \"bk\": %d, \"binned_smem_kb\": %u, \"R\": %u, \"occ_bin\": %d, \"occ_app\": %d, \"grid_app\": %d, "
+           "\"bin_ms\": %.4f, \"apply_ms\": %.4f, \"add\": %.2f, \"filter_hash\": \"%s\", \"match\": %s}\n",
+           name, NT, BK, range_kb, R, occ_bin, occ_app, ga, tb[tb.size() / 2], ta[ta.size() / 2], c.n / tt[tt.size() / 2] / 1e6, hs,
+           strcmp(hs, want_hash) == 0 ? "true" : "false");
+    fflush(stdout);
+}
+
 int main(int argc, char** argv)
 {
     Ctx c{};
@@ -116,6 +264,22 @@ int main(int argc, char** argv)
     CK(cudaDeviceSynchronize());
     CK(cudaEventCreate(&c.e0));
     CK(cudaEventCreate(&c.e1));
+    if (argc > 1 && strcmp(argv[1], "binned") == 0) {
+        using SBF8 = Cfg<V_SBF, 64, 2, 8, 0, 1, 4, 1, 0>;
+        const char* h8 = "87f62ba45aed76b6";
+        for (uint32_t kb : {32u, 64u}) {
+            run_binned<SBF8, 256, 8>(c, "SBF256/64 k8", kb, h8);
+            run_binned<SBF8, 512, 8>(c, "SBF256/64 k8", kb, h8);
+            run_binned<SBF8, 512, 16>(c, "SBF256/64 k8", kb, h8);
+            run_binned<SBF8, 1024, 8>(c, "SBF256/64 k8", kb, h8);
+            run_binned<SBF8, 1024, 4>(c, "SBF256/64 k8", kb, h8);
+        }
+        run_binned<Cfg<V_SBF, 64, 2, 16, 0, 1, 4, 1, 0>, 512, 16>(c, "SBF256/64 k16", 64, "be95309645de7752");
+        run_binned<Cfg<V_BBF, 64, 2, 16, 0, 1, 4, 1, 0>, 512, 16>(c, "BBF256/64 k16", 64, "b790872c89131856");
+        run_binned<Cfg<V_RBBF, 64, 0, 16, 0, 1, 1, 1, 0>, 512, 16>(c, "RBBF64 k16", 64, "1e185dd3897acc25");
+        run_binned<Cfg<V_CSBF, 32, 3, 8, 2, 1, 8, 1, 0>, 512, 16>(c, "CSBF256/32 z2 k8", 64, "a59a64f3e2297f08");
+        return 0;
+    }
     //                 V      S  lgs K  Z  TH PHI KPT HV
     run<Cfg<V_SBF, 64, 2, 8, 0, 4, 1, 4, 0>, Cfg<V_SBF, 64, 2, 8, 0, 1, 4, 4, 0>>(c, "SBF256/64 k8");
     run<Cfg<V_SBF, 64, 2, 16, 0, 4, 1, 4, 0>, Cfg<V_SBF, 64, 2, 16, 0, 1, 4, 4, 0>>(c, "SBF256/64 k16");
