@@ -294,9 +294,11 @@ def run_ours(a, cfg, rank, world, local_rank):
         graph = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
         cap.wait_stream(stream)
+        lc0 = bf.bf_launch_count()
         with torch.cuda.stream(cap):
             with torch.cuda.graph(graph, stream=cap):
                 step()
+        graph_launches = bf.bf_launch_count() - lc0  # our kernels captured in one step
         stream.wait_stream(cap)
         graph.replay()
         torch.cuda.synchronize()
@@ -312,7 +314,7 @@ def run_ours(a, cfg, rank, world, local_rank):
         torch.cuda.synchronize()
     launches = bf.bf_launch_count() - launches0
     if graph is not None:
-        launches = 2 * a.steps  # the graph replays the two captured kernels per step
+        launches = graph_launches * a.steps  # each replay runs the captured kernels of one step
     ms_local = t_start.elapsed_time(t_end) / a.steps
     t_add = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
     t_con = statistics.mean(e[3].elapsed_time(e[4]) for e in evs)

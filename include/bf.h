@@ -89,7 +89,11 @@ bf_filter* bf_create_seeded(uint64_t m_bits, uint32_t k, uint32_t block_bits,
  * one").  keys: device pointer to n uint64.  Sets the k pattern bits of every
  * key with red.global.or; concurrent bf_add calls on any streams are safe
  * (OR commutes; binned adds -- bf_set_add_mode -- share the filter's
- * scratch and are ordered among themselves by the library).  Idempotent. */
+ * scratch and are ordered among themselves by the library, except while
+ * `stream` is being captured into a CUDA graph: then the caller orders a
+ * captured binned add against binned adds of the same filter on other
+ * streams).  The first binned add allocates the scratch (cudaMalloc), so it
+ * must not be the one captured.  Idempotent. */
 int bf_add(bf_filter* f, const uint64_t* keys, uint64_t n, void* stream);
 
 /* Bulk lookup ("If any bit is zero, the element is certainly not in the

@@ -343,13 +343,15 @@ static int contains_one(const bfo_filter* f, uint64_t key)
 /* threading: contiguous key ranges, one POSIX thread each.  For contains the
  * ranges are multiples of 32 keys so no two threads write one result word. */
 typedef struct {
-    int op; /* 0 add, 1 contains, 2 add_range */
+    int op; /* 0 add, 1 contains, 2 add_range, 3 contains_range */
     bfo_filter* f;
     const uint64_t* keys;
     uint64_t lo, hi;
     uint32_t* out;
     uint64_t blk_lo, blk_hi;
     uint8_t* range_out;
+    const uint8_t* range_in;
+    int8_t* range_res;
 } job_t;
 
 static void range_add_one(const job_t* j, uint64_t key)
@@ -361,6 +363,18 @@ static void range_add_one(const job_t* j, uint64_t key)
         set_bit_atomic(j->range_out, (blk - j->blk_lo) * j->f->B + pos[t]);
 }
 
+/* contains against the bytes of blocks [blk_lo, blk_hi) only (the key
+ * is absent iff one of its k bits is zero); -1 for keys outside the range */
+static int8_t range_contains_one(const job_t* j, uint64_t key)
+{
+    uint64_t blk, pos[32];
+    bfo_pattern(j->f, key, &blk, pos);
+    if (blk < j->blk_lo || blk >= j->blk_hi) return -1;
+    for (uint32_t t = 0; t < j->f->k; ++t)
+        if (!get_bit(j->range_in, (blk - j->blk_lo) * j->f->B + pos[t])) return 0;
+    return 1;
+}
+
 static void* run_job(void* arg)
 {
     job_t* j = (job_t*)arg;
@@ -369,8 +383,10 @@ static void* run_job(void* arg)
     } else if (j->op == 1) {
         for (uint64_t i = j->lo; i < j->hi; ++i)
             if (contains_one(j->f, j->keys[i])) j->out[i >> 5] |= 1u << (i & 31);
-    } else {
+    } else if (j->op == 2) {
         for (uint64_t i = j->lo; i < j->hi; ++i) range_add_one(j, j->keys[i]);
+    } else {
+        for (uint64_t i = j->lo; i < j->hi; ++i) j->range_res[i] = range_contains_one(j, j->keys[i]);
     }
     return NULL;
 }
@@ -443,6 +459,25 @@ int bfo_add_range(const bfo_filter* f, const uint64_t* keys, uint64_t n,
     j.blk_lo = blk_lo;
     j.blk_hi = blk_hi;
     j.range_out = out;
+    return run(j, n, nthreads);
+}
+
+int bfo_contains_range(const bfo_filter* f, const uint64_t* keys, uint64_t n,
+                       uint64_t blk_lo, uint64_t blk_hi, const uint8_t* range_bytes,
+                       int8_t* out, int nthreads)
+{
+    if (!f || f->variant == BFO_CBF || blk_lo > blk_hi || blk_hi > f->b || (n && (!keys || !out)) ||
+        !range_bytes)
+        return BFO_EINVAL;
+    job_t j;
+    memset(&j, 0, sizeof j);
+    j.op = 3;
+    j.f = (bfo_filter*)f;
+    j.keys = keys;
+    j.blk_lo = blk_lo;
+    j.blk_hi = blk_hi;
+    j.range_in = range_bytes;
+    j.range_res = out;
     return run(j, n, nthreads);
 }
 

@@ -104,6 +104,15 @@ int bfo_contains(const bfo_filter* f, const uint64_t* keys, uint64_t n,
 int bfo_add_range(const bfo_filter* f, const uint64_t* keys, uint64_t n,
                   uint64_t blk_lo, uint64_t blk_hi, uint8_t* out, int nthreads);
 
+/* Range-restricted contains: out[i] = -1 if keys[i]'s block lies outside
+ * [blk_lo, blk_hi), else contains(keys[i]) tested bit by bit against
+ * range_bytes = bits[blk_lo*B/8 .. blk_hi*B/8) of the full filter (e.g. what
+ * bfo_add_range produced).  Checks lookups of multi-GiB GPU filters on sampled
+ * ranges. */
+int bfo_contains_range(const bfo_filter* f, const uint64_t* keys, uint64_t n,
+                       uint64_t blk_lo, uint64_t blk_hi, const uint8_t* range_bytes,
+                       int8_t* out, int nthreads);
+
 /* Number of set bits in the filter. */
 uint64_t bfo_popcount(const bfo_filter* f);
 

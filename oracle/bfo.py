@@ -61,6 +61,8 @@ def lib():
             L.bfo_contains.argtypes = [vp, vp, u64, vp, i32]
             L.bfo_add_range.restype = i32
             L.bfo_add_range.argtypes = [vp, vp, u64, u64, u64, vp, i32]
+            L.bfo_contains_range.restype = i32
+            L.bfo_contains_range.argtypes = [vp, vp, u64, u64, u64, vp, vp, i32]
             L.bfo_set_scheme.restype = i32
             L.bfo_set_scheme.argtypes = [vp, i32]
             L.bfo_popcount.restype = u64
@@ -160,6 +162,20 @@ class OracleFilter:
                                  out.ctypes.data, threads)
         if rc:
             raise RuntimeError(f"bfo_add_range rc={rc}")
+        return out
+
+    def contains_range(self, keys, blk_lo: int, blk_hi: int, range_bytes, threads: int = 1) -> np.ndarray:
+        """int8 per key: -1 if its block is outside [blk_lo, blk_hi), else
+        contains(key) against range_bytes (bytes of those blocks)."""
+        ks = _keys(keys)
+        rb = np.ascontiguousarray(range_bytes, dtype=np.uint8)
+        if rb.size != (blk_hi - blk_lo) * self.B // 8:
+            raise ValueError("range_bytes does not cover [blk_lo, blk_hi)")
+        out = np.empty(ks.size, dtype=np.int8)
+        rc = lib().bfo_contains_range(self._p, ks.ctypes.data, ks.size, blk_lo, blk_hi,
+                                      rb.ctypes.data, out.ctypes.data, threads)
+        if rc:
+            raise RuntimeError(f"bfo_contains_range rc={rc}")
         return out
 
     def bytes(self) -> np.ndarray:

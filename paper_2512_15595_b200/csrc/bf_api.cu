@@ -494,14 +494,21 @@ static int binned_add(bf_filter* f, const uint64_t* keys, uint64_t n, cudaStream
 {
     std::lock_guard<std::mutex> g(f->mu);
     cudaError_t e = cudaSuccess;
+    // Under CUDA graph capture the cross-stream ordering event cannot be used
+    // (waiting on work recorded outside the capture invalidates it): the
+    // captured adds are ordered by the graph, and the caller orders them
+    // against binned adds of this filter on other streams (include/bf.h).
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if ((e = cudaStreamIsCapturing(st, &cs)) != cudaSuccess) return cuda_fail(e, "binned add: capture status");
+    const bool capturing = cs != cudaStreamCaptureStatusNone;
     if (!f->scratch_done) {
         if ((e = cudaEventCreateWithFlags(&f->scratch_done, cudaEventDisableTiming)) != cudaSuccess)
             return cuda_fail(e, "binned add: event");
-    } else if ((e = cudaStreamWaitEvent(st, f->scratch_done, 0)) != cudaSuccess) {
+    } else if (!capturing && (e = cudaStreamWaitEvent(st, f->scratch_done, 0)) != cudaSuccess) {
         return cuda_fail(e, "binned add: wait for the previous binned add");
     }
     int rc = binned_add_locked(f, keys, n, st, bin_fn, apply_fn);
-    if (rc == BF_OK && (e = cudaEventRecord(f->scratch_done, st)) != cudaSuccess)
+    if (rc == BF_OK && !capturing && (e = cudaEventRecord(f->scratch_done, st)) != cudaSuccess)
         return cuda_fail(e, "binned add: event record");
     return rc;
 }

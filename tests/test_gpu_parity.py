@@ -628,10 +628,12 @@ def test_hybrid_add_matches_oracle(bflib, cuda, cfg):
     assert np.array_equal(_gpu_bytes(f), o.bytes())
 
 
-def test_cuda_graph_capture_and_replay(bflib, cuda):
+@pytest.mark.parametrize("binned", [False, True], ids=["direct", "binned"])
+def test_cuda_graph_capture_and_replay(bflib, cuda, binned):
     """bf_clear + bf_add + bf_contains are stream-ordered and capture-safe:
     one captured step replayed three times gives the oracle's bits and
-    answers (bench.py times such replays)."""
+    answers (bench.py times such replays), for the direct add and for the
+    binned add (bin + one apply launch per range) that configs[2] uses."""
     import torch
     bf = bflib
     n = (1 << 18) + 7
@@ -639,6 +641,8 @@ def test_cuda_graph_capture_and_replay(bflib, cuda):
     o = OracleFilter(3, 1 << 22, B=256, S=64, k=8)
     o.add(keys)
     f = bf.Filter(1 << 22, 8, 256, 64, "SBF")
+    if binned:
+        f.set_add_mode(bf.BF_ADD_BINNED, 1 << 16, 0)  # 8 ranges
     kd = _to_dev(torch, keys, cuda)
     out = torch.empty((n + 31) // 32, dtype=torch.int32, device=cuda)
     f.add(kd)  # warm-up (lazy module loading) outside the capture
@@ -654,6 +658,7 @@ def test_cuda_graph_capture_and_replay(bflib, cuda):
         out.fill_(0)
         g.replay()
     torch.cuda.synchronize()
+    assert f.add_mode()[1] == int(binned)
     assert np.array_equal(_gpu_bytes(f), o.bytes())
     assert np.array_equal(out.cpu().numpy().view(np.uint32), o.contains(keys))
 
