@@ -455,31 +455,68 @@ def run_probes(bf, torch, f, keys, out, cfg, reps=5):
 
 
 def run_e2e(bf, torch, f, keys, cfg, a, world, steps=3):
-    """Same metric through the public C-ABI host-buffer calls: keys start in
-    pinned host memory and results end there (copies inside the timed region)."""
+    """Same metric end to end through the public API, inputs and results in
+    pinned host memory, every copy inside the timed region.
+
+    Main figure: the step's key batch crosses PCIe once -- it is copied to
+    the device in 8 chunks on a copy stream, each chunk added as soon as it
+    lands (H2D of chunk c+1 overlaps the add of chunk c), then contains runs
+    over the resident batch and the packed result bits come back (what a
+    user inserting and then querying a batch does with Filter.add /
+    Filter.contains).  Also reported: the bf_add_host + bf_contains_host
+    path, which stages the keys through the library once per call (2x H2D)."""
     n = keys.numel()
     hk = torch.empty(n, dtype=torch.int64, pin_memory=True)
     hk.copy_(keys.cpu())
     hout = torch.empty((n + 31) // 32, dtype=torch.int32, pin_memory=True)
+    kdev = torch.empty_like(keys)
+    dout = torch.empty((n + 31) // 32, dtype=torch.int32, device=keys.device)
     st = torch.cuda.current_stream()
+    cs = torch.cuda.Stream()
+    nchunk = 8
+    bounds = [(n * c // nchunk) // 4 * 4 for c in range(nchunk)] + [n]  # 32-byte aligned chunks
+    evs = [torch.cuda.Event() for _ in range(nchunk)]
 
     def one():
+        f.clear()
+        cs.wait_stream(st)  # the previous step's contains has read kdev
+        for c in range(nchunk):
+            lo, hi = bounds[c], bounds[c + 1]
+            with torch.cuda.stream(cs):
+                kdev[lo:hi].copy_(hk[lo:hi], non_blocking=True)
+                evs[c].record(cs)
+            st.wait_event(evs[c])
+            f.add(kdev[lo:hi])
+        f.contains(kdev, dout)
+        hout.copy_(dout, non_blocking=True)
+
+    def one_host():
         f.clear()
         f.add_host(hk)
         f.contains_host(hk, hout)
 
-    one()
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        one()
+    def timed(fn):
+        fn()
         torch.cuda.synchronize()
-        ts.append(time.perf_counter() - t0)
-    t = statistics.median(ts)
+        ts = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts)
+
+    t = timed(one)
+    assert int((hout != -1).sum().item()) == 0 or n % 32, "false negative in the e2e result"
+    th = timed(one_host)
     return {"value": round(2 * n * world / t / 1e9, 3), "unit": "Gkeys/s",
-            "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": ((n + 31) // 32) * 4,
-            "ms_per_step": round(t * 1e3, 3), "path": "bf_add_host + bf_contains_host (pinned host buffers)"}
+            "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": ((n + 31) // 32) * 4,
+            "ms_per_step": round(t * 1e3, 3),
+            "path": "pinned host keys -> 8 chunked H2D copies overlapped with Filter.add; Filter.contains; "
+                    "D2H of the packed result bits (wall clock, synchronized)",
+            "host_call_path": {"value": round(2 * n * world / th / 1e9, 3), "unit": "Gkeys/s",
+                               "h2d_bytes_per_step": 2 * n * 8, "ms_per_step": round(th * 1e3, 3),
+                               "path": "bf_add_host + bf_contains_host (keys staged once per call)"}}
 
 
 def main():
