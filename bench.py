@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="keys per rank (override)")
     ap.add_argument("--m-bits", dest="m_bits", type=int, default=None, help="filter bits (override)")
     ap.add_argument("--range-mib", type=int, default=0, help="binned add: filter MiB per range (0: library default)")
-    ap.add_argument("--merge", choices=["alltoall", "allgather", "nvls"], default="alltoall")
+    ap.add_argument("--merge", choices=["alltoall", "allgather", "nvls", "p2p"], default="alltoall")
     ap.add_argument("--add-mode", choices=["auto", "direct", "binned"], default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

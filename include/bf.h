@@ -294,6 +294,39 @@ int bf_mcast_mc_ptr(bf_mcast* m, void** mc_ptr, uint64_t* size);
 int bf_mcast_or_reduce(bf_mcast* m, uint32_t rank, uint64_t bytes, void* stream);
 void bf_mcast_destroy(bf_mcast* m);
 
+/* ---- OR merge over peer memory (construction's exchange) ----
+ *
+ * The same merge as E1/E2/E4 -- every rank's filter becomes the bitwise OR of
+ * the P partial filters -- as ONE kernel per rank over NVLink
+ * peer mappings instead of NCCL transfers plus a separate OR-fold pass: rank
+ * r loads its 1/P slice of all P filters straight from the peers' memory,
+ * ORs them and stores the result into all P filters (a reduce-scatter by OR
+ * fused with the all-gather).
+ *
+ * bf_ipc_handle: the BF_IPC_HANDLE_BYTES-byte CUDA IPC handle of the device
+ *   allocation starting at dev_ptr (use bf_data's pointer: the filter's
+ *   allocation base).  Exchange the blobs between the ranks (any transport).
+ * bf_ipc_open: map a peer's allocation into this process (peer access is
+ *   enabled lazily); *dev_ptr_out is valid on the caller's current device.
+ *   Opening a handle exported by the calling process itself fails (CUDA IPC
+ *   is between processes): use the local pointer.  bf_ipc_close unmaps.
+ * bf_p2p_or_merge: peers is a HOST array of nranks device pointers to equal
+ *   `bytes`-long filters (peers[rank] this rank's own, the others opened with
+ *   bf_ipc_open), 16-byte aligned, bytes % 4 == 0, 1 <= nranks <=
+ *   BF_P2P_MAX_RANKS.  Enqueues on `stream` the OR of 16-byte elements
+ *   [rank*E/P, (rank+1)*E/P) (E = bytes/16; the last rank also takes the
+ *   4-byte tail words) of all filters into all filters.  The caller brackets
+ *   it with a barrier that orders it after every rank's adds and one that
+ *   orders every rank's later reads after all ranks' merges (a stream-ordered
+ *   NCCL collective on a 1-element tensor does both; dist.P2pMerger).
+ *   BF_EINVAL for bad arguments; BF_ECUDA on a launch failure. */
+#define BF_IPC_HANDLE_BYTES 64
+#define BF_P2P_MAX_RANKS 16
+int bf_ipc_handle(const void* dev_ptr, void* handle_out);
+int bf_ipc_open(const void* handle, void** dev_ptr_out);
+int bf_ipc_close(void* dev_ptr);
+int bf_p2p_or_merge(void* const* peers, uint32_t nranks, uint32_t rank, uint64_t bytes, void* stream);
+
 /* Number of kernels this library has launched since load (all entry points).
  * Lets callers prove the CUDA path ran. */
 uint64_t bf_launch_count(void);

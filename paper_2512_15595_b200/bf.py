@@ -73,6 +73,10 @@ _SIGS = {
     "bf_mcast_mc_ptr": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_u64)]),
     "bf_mcast_or_reduce": (_i32, [_vp, _u32, _u64, _vp]),
     "bf_mcast_destroy": (None, [_vp]),
+    "bf_ipc_handle": (_i32, [_vp, _vp]),
+    "bf_ipc_open": (_i32, [_vp, C.POINTER(_vp)]),
+    "bf_ipc_close": (_i32, [_vp]),
+    "bf_p2p_or_merge": (_i32, [_vp, _u32, _u32, _u64, _vp]),
     "bf_launch_count": (_u64, []),
     "bf_last_error": (C.c_char_p, [C.POINTER(_i32)]),
     "bf_version": (C.c_char_p, []),
@@ -283,6 +287,34 @@ def bf_mcast_or_reduce(m: int, rank: int, nbytes: int, stream=None) -> None:
 
 def bf_mcast_destroy(m: int) -> None:
     _lib.bf_mcast_destroy(m)
+
+
+BF_IPC_HANDLE_BYTES, BF_P2P_MAX_RANKS = 64, 16
+
+
+def bf_ipc_handle(dev_ptr: int) -> bytes:
+    """64-byte CUDA IPC handle of the allocation starting at dev_ptr."""
+    blob = C.create_string_buffer(BF_IPC_HANDLE_BYTES)
+    _check(_lib.bf_ipc_handle(dev_ptr, blob))
+    return blob.raw
+
+
+def bf_ipc_open(handle: bytes) -> int:
+    """Map a peer process's allocation; returns a device pointer."""
+    blob = C.create_string_buffer(handle, BF_IPC_HANDLE_BYTES)
+    p = _vp()
+    _check(_lib.bf_ipc_open(blob, C.byref(p)))
+    return p.value
+
+
+def bf_ipc_close(dev_ptr: int) -> None:
+    _check(_lib.bf_ipc_close(dev_ptr))
+
+
+def bf_p2p_or_merge(peers: list[int], rank: int, nbytes: int, stream=None) -> None:
+    """OR slice `rank` of all peers' filters into all of them (one kernel)."""
+    arr = (_vp * len(peers))(*peers)
+    _check(_lib.bf_p2p_or_merge(arr, len(peers), rank, nbytes, _stream(stream)))
 
 
 def bf_launch_count() -> int:

@@ -15,6 +15,12 @@
      folded), OR-fold it, then all_gather the merged ranges.  Receives
      2*(P-1)/P*M bytes per rank, 4x less than E1 at P=8.
 
+  E4 ``nvls``  in-switch OR over NVLink SHARP (NvlsMerger, bf_mcast_*).
+  p2p ``p2p``  one kernel per rank over CUDA-IPC peer mappings (P2pMerger,
+     bf_p2p_or_merge): rank r loads its 1/P slice of every peer's partial
+     straight over NVLink, ORs and stores it into every peer -- the
+     reduce-scatter by OR and the all-gather fused, no staging, no fold pass.
+
 The functions take the filter's word array as a flat uint8 tensor (a view of
 bf_data) and an ``or_fold(dst, src2d)`` callable; the default is the CUDA
 kernel.  (CPU/gloo tests pass a CPU fold to check the chunk and offset
@@ -144,7 +150,74 @@ def merge_nvls(words: torch.Tensor, group=None) -> None:
     mg.merge(words)
 
 
-MERGES = {"allgather": merge_allgather, "alltoall": merge_alltoall, "nvls": merge_nvls}
+class P2pMerger:
+    """OR merge over NVLink peer memory (bf_p2p_or_merge, include/bf.h).
+
+    Collective constructor over the group: every rank exports the CUDA IPC
+    handle of its filter allocation (``words`` must be the filter's whole
+    word array, bf_data's view), all_gathers the handles and maps every
+    peer's filter.  ``merge()``: a stream-ordered barrier (all_reduce of one
+    element: every rank's adds are done), one kernel per rank that ORs its
+    1/P slice of all P filters and writes it into all P, and a second barrier
+    (every rank's stores into this filter are done before it is read).  No
+    staging buffer, no separate fold pass; per rank (P-1)/P*M bytes read from
+    peers and (P-1)/P*M written to them."""
+
+    def __init__(self, words: torch.Tensor, group=None):
+        from . import bf
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.P > bf.BF_P2P_MAX_RANKS:
+            raise ValueError(f"p2p merge supports at most {bf.BF_P2P_MAX_RANKS} ranks")
+        self.words = words
+        self.nbytes = words.numel()
+        mine = bf.bf_ipc_handle(words.data_ptr())
+        handles = [None] * self.P
+        dist.all_gather_object(handles, mine, group=group)
+        self.peers = []
+        self._opened = []
+        for q, h in enumerate(handles):
+            if q == self.rank:
+                self.peers.append(words.data_ptr())
+            else:
+                p = bf.bf_ipc_open(h)
+                self._opened.append(p)
+                self.peers.append(p)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=words.device)
+
+    def merge(self, words: torch.Tensor | None = None) -> None:
+        from . import bf
+        if words is not None and words.data_ptr() != self.words.data_ptr():
+            raise ValueError("P2pMerger merges the filter it was built for")
+        dist.all_reduce(self.flag, group=self.group)  # every rank's adds are done
+        bf.bf_p2p_or_merge(self.peers, self.rank, self.nbytes)
+        dist.all_reduce(self.flag, group=self.group)  # every rank's stores are done
+
+    def close(self):
+        from . import bf
+        if self._opened:
+            if self.words.is_cuda:
+                torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+            for p in self._opened:
+                bf.bf_ipc_close(p)
+            self._opened = []
+
+
+_p2p_cache: dict = {}
+
+
+def merge_p2p(words: torch.Tensor, group=None) -> None:
+    """P2P merge as a MERGES entry: one P2pMerger per (group, filter), kept."""
+    key = (id(group), words.data_ptr(), words.numel())
+    mg = _p2p_cache.get(key)
+    if mg is None:
+        mg = _p2p_cache[key] = P2pMerger(words, group)
+    mg.merge(words)
+
+
+MERGES = {"allgather": merge_allgather, "alltoall": merge_alltoall, "nvls": merge_nvls, "p2p": merge_p2p}
 
 
 def build_replicated(filt, keys: torch.Tensor, strategy: str = "alltoall", group=None) -> None:
