@@ -2,7 +2,7 @@
 """Summarise ncu output into profiles/ (tracked).
 
     python tools/ncu_summary.py launches gpurun_out/launches_r1.csv  > profiles/r1_launches.md
-    python tools/ncu_summary.py full gpurun_out/prof_r1.ncu-rep        > profiles/r1_ncu_full.md
+    python tools/ncu_summary.py full gpurun_out/prof_r1.ncu-rep [N_KEYS] > profiles/r1_ncu_full.md
 """
 from __future__ import annotations
 
@@ -51,7 +51,18 @@ def launches(path):
         print(f"| `{k[:110]}` | {len(v)} | {sum(v) / len(v):.1f} | {sum(v):.1f} | {100 * sum(v) / tot:.1f}% |")
 
 
-def full(path):
+PER_KEY = [  # (metric, label, multiplier): per-key evidence (SURVEY 8(d) "ncu evidence per design choice")
+    ("smsp__inst_executed.sum", "thread instructions / key", 32),
+    ("lts__t_requests_srcunit_tex_op_read.sum", "L2 read requests / key", 1),
+    ("lts__t_requests_srcunit_tex_op_red.sum", "L2 RED requests / key (1.0 = Θ lanes coalesced into one request)", 1),
+    ("lts__t_sectors_srcunit_tex_op_red.sum", "L2 RED sectors / key", 1),
+    ("dram__bytes_read.sum", "DRAM bytes read / key", 1),
+    ("dram__bytes_write.sum", "DRAM bytes written / key", 1),
+]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "inst": 1, "request": 1, "sector": 1}
+
+
+def full(path, n_keys=None):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, units = rows[0], rows[1]
@@ -65,6 +76,15 @@ def full(path):
             if key in h:
                 i = h.index(key)
                 print(f"| {label} (`{key}`) | {r[i]} {units[i]} |")
+        if n_keys:
+            for key, label, mul in PER_KEY:
+                if key in h:
+                    i = h.index(key)
+                    try:
+                        v = float(r[i].replace(",", "")) * SCALE.get(units[i], 1) * mul / float(n_keys)
+                    except ValueError:
+                        continue
+                    print(f"| {label} (n = {int(n_keys)}) | {v:.3f} |")
         items = []
         for i, c in enumerate(h):
             if c.startswith("smsp__pcsamp_warps_issue_stalled_") and not c.endswith("_not_issued"):
@@ -104,4 +124,4 @@ if __name__ == "__main__":
     if sys.argv[1] == "traffic":
         traffic(sys.argv[2], sys.argv[3], sys.argv[4])
     else:
-        {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+        {"launches": launches, "full": full}[sys.argv[1]](*sys.argv[2:])
