@@ -2,7 +2,7 @@
 """Benchmark of the bulk add / contains hot path (arXiv 2512.15595) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c2|c1|c3] [--variant SBF --B 256 --S 64 --k 8 --z 0]
+                    [--config c2|c1|c3|c5] [--variant SBF --B 256 --S 64 --k 8 --z 0]
 
 One step = one pass of the whole hot path over one batch of synthetic keys
 resident in HBM (BASELINE.json configs[1] by default: a 32 MiB L2-resident
@@ -39,6 +39,11 @@ CONFIGS = {
     # configs[2]: HBM-resident 8 GiB filter, 2^32 keys.
     "c3": dict(workload="configs[2]: HBM-resident 8 GiB filter, 2^32 keys, SBF B=256 S=64 k=8",
                m_bits=1 << 36, n=1 << 32, variant="SBF", B=256, S=64, k=8, z=0, residency="HBM"),
+    # configs[4]: one rank's share of the 8-GPU job -- a 32 GiB replica and
+    # 2^34 / 8 = 2^31 keys per rank (weak scaling: N ranks build from N*2^31
+    # keys, merge, and look up their own shard).
+    "c5": dict(workload="configs[4] per rank: 32 GiB replica, 2^31 keys per rank (2^34 at 8 GPUs), SBF B=256 S=64 k=8",
+               m_bits=1 << 38, n=1 << 31, variant="SBF", B=256, S=64, k=8, z=0, residency="HBM"),
 }
 
 VARIANT_IDS = {"BBF": 1, "RBBF": 2, "SBF": 3, "CSBF": 4}

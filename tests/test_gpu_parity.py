@@ -679,3 +679,24 @@ def test_default_layouts(bflib, cuda, cfg, add_l, con_l):
     for op, want in ((0, add_l), (1, con_l)):
         lay = f.layout(op)
         assert (lay["theta"], lay["phi"], lay["kpt"], lay["specialized"]) == (*want, 1), (op, lay)
+
+
+def test_auto_add_path_threshold(bflib, cuda):
+    """BF_ADD_AUTO takes the binned path for filters >= 96 MiB once the batch
+    has one key per 64 filter bytes (include/bf.h), the direct path below;
+    both give the oracle's bits on a sampled range."""
+    import torch
+    bf = bflib
+    m = 1 << 31  # 256 MiB
+    nb = (m // 8) // 64
+    f = bf.Filter(m, 8, 256, 64, "SBF")
+    for n, want in ((nb - 1, 0), (nb, 1)):
+        f.clear()
+        kd = torch.empty(n, dtype=torch.int64, device=cuda)
+        bf.bf_keygen(kd, n, 5)
+        f.add(kd)
+        torch.cuda.synchronize()
+        assert f.add_mode() == (bf.BF_ADD_AUTO, want), n
+        o = OracleFilter(3, m, B=256, S=64, k=8, allocate=False)
+        lo, hi = o.b // 2, o.b // 2 + 4096
+        assert np.array_equal(_gpu_bytes(f)[lo * 32:hi * 32], o.add_range(synth.keys(5, n), lo, hi, threads=os.cpu_count()))
