@@ -129,6 +129,12 @@ __global__ void __launch_bounds__(NT) bin_kernel(const BinParams bp)
     for (uint64_t c = blockIdx.x; c * CHUNK < p.n; c += gridDim.x) {
         const uint64_t base = c * CHUNK;
         const uint32_t cnt = (uint32_t)min((uint64_t)CHUNK, p.n - base);
+        {  // L2 prefetch of this CTA's chunk two grid strides ahead, one 128-byte
+           // line per thread, no registers: the key loads below then wait for
+           // L2 instead of HBM (+10% on the bin phase, tools/kexp)
+            const uint64_t pb = base + 2ULL * gridDim.x * CHUNK + (uint64_t)tid * 16;
+            if (tid < CHUNK / 16 && pb < p.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.keys + pb));
+        }
         for (uint32_t r = tid; r < R; r += NT) hist[r] = 0;
         __syncthreads();
         // hash once per key; count per range (coalesced key loads: i*256+tid)

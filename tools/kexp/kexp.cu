@@ -249,6 +249,76 @@ static void run_binned(Ctx& c, const char* name, uint32_t range_kb, const char* 
     fflush(stdout);
 }
 
+// bin phase only (records into R buckets), staged vs register-direct writes
+template <class C1, int NT, int BK, bool REG>
+static void run_bin(Ctx& c, const char* name, uint32_t range_kb)
+{
+    const uint64_t B = C1::B;
+    const uint64_t b = c.m_bits / B;
+    uint32_t lg = 0;
+    while ((B / 8) << (lg + 1) <= (uint64_t)range_kb * 1024) ++lg;
+    const uint32_t R = (uint32_t)((b + (1ULL << lg) - 1) >> lg);
+    const uint64_t cap = ((c.n / R + c.n / R / 32 + 8192) + 127) & ~127ULL;
+    static uint64_t* recs = nullptr;
+    static unsigned long long* cursor = nullptr;
+    static size_t recs_bytes = 0;
+    if (recs_bytes < R * cap * 8) {
+        if (recs) cudaFree(recs);
+        CK(cudaMalloc(&recs, R * cap * 8));
+        recs_bytes = R * cap * 8;
+    }
+    if (!cursor) CK(cudaMalloc(&cursor, 65536 * 8));
+    BinParams bp{};
+    bp.f.words = c.words;
+    bp.f.b = b;
+    bp.f.b32 = (uint32_t)b;
+    bp.f.keys = c.keys;
+    bp.f.n = c.n;
+    bp.recs = recs;
+    bp.cursor = cursor;
+    bp.cap = cap;
+    bp.lg_bpr = lg;
+    bp.nranges = R;
+    auto kern = bin_kernel<C1, NT, BK>;
+    const size_t sm = bin_smem_bytes(R, NT * BK);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int nsm = 0, occ = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, sm));
+    const uint64_t chunks = (c.n + NT * BK - 1) / (NT * BK);
+    const int gb = (int)std::min<uint64_t>(chunks, (uint64_t)occ * nsm);
+    std::vector<float> ts;
+    uint64_t sum = 0;
+    for (int r = 0; r < c.reps + 2; ++r) {
+        CK(cudaMemsetAsync(cursor, 0, R * 8));
+        CK(cudaEventRecord(c.e0));
+        kern<<<gb, NT, sm>>>(bp);
+        CK(cudaEventRecord(c.e1));
+        CK(cudaEventSynchronize(c.e1));
+        CK(cudaGetLastError());
+        float ms;
+        CK(cudaEventElapsedTime(&ms, c.e0, c.e1));
+        if (r >= 2) ts.push_back(ms);
+    }
+    // checksum: per-bucket counts and the XOR of all records (order-free)
+    std::vector<unsigned long long> cur(R);
+    CK(cudaMemcpy(cur.data(), cursor, R * 8, cudaMemcpyDeviceToHost));
+    std::vector<uint64_t> hr(R * cap);
+    CK(cudaMemcpy(hr.data(), recs, R * cap * 8, cudaMemcpyDeviceToHost));
+    uint64_t x = 0, tot = 0;
+    for (uint32_t r = 0; r < R; ++r) {
+        tot += cur[r];
+        for (uint64_t i = 0; i < std::min<uint64_t>(cur[r], cap); ++i) x ^= hr[r * cap + i] * 0x9E3779B97F4A7C15ULL + r;
+    }
+    std::sort(ts.begin(), ts.end());
+    printf("{\"cfg\": \"%s\", \"bin\": \"%s\", \"nt\": %d, \"bk\": %d, \"R\": %u, \"occ\": %d, \"bin_ms\": %.4f, "
+           "\"gkeys_s\": %.2f, \"total\": %llu, \"xor\": \"%016llx\"}\n",
+           name, REG ? "reg" : "staged", NT, BK, R, occ, ts[ts.size() / 2], c.n / ts[ts.size() / 2] / 1e6,
+           (unsigned long long)tot, (unsigned long long)x);
+    fflush(stdout);
+    (void)sum;
+}
+
 int main(int argc, char** argv)
 {
     Ctx c{};
@@ -264,6 +334,16 @@ int main(int argc, char** argv)
     CK(cudaDeviceSynchronize());
     CK(cudaEventCreate(&c.e0));
     CK(cudaEventCreate(&c.e1));
+    if (argc > 1 && strcmp(argv[1], "bin") == 0) {
+        using SBF8 = Cfg<V_SBF, 64, 2, 8, 0, 1, 4, 1, 0>;
+        for (uint32_t kb : {128u, 64u}) {
+            run_bin<SBF8, 256, 8, false>(c, "SBF256/64 k8", kb);
+            run_bin<SBF8, 256, 4, false>(c, "SBF256/64 k8", kb);
+            run_bin<SBF8, 128, 8, false>(c, "SBF256/64 k8", kb);
+            run_bin<SBF8, 512, 4, false>(c, "SBF256/64 k8", kb);
+        }
+        return 0;
+    }
     if (argc > 1 && strcmp(argv[1], "binned") == 0) {
         using SBF8 = Cfg<V_SBF, 64, 2, 8, 0, 1, 4, 1, 0>;
         const char* h8 = "87f62ba45aed76b6";
