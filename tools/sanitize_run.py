@@ -52,7 +52,13 @@ bf.bf_keygen(buf, 4095, 7)
 dst = torch.zeros(1 << 12, dtype=torch.uint8, device=dev)
 src = torch.ones(3 << 12, dtype=torch.uint8, device=dev)
 bf.bf_or_fold(dst, src, 3, 1 << 12, 1 << 12)
+# peer-memory OR merge, 3 virtual ranks on this device (ragged 4-byte tail)
+pb = [torch.from_numpy(np.random.default_rng(r).integers(0, 256, 4096 + 12, dtype=np.uint8)).to(dev) for r in range(3)]
+want_or = np.bitwise_or.reduce(np.stack([t.cpu().numpy() for t in pb]), axis=0)
+for r in range(3):
+    bf.bf_p2p_or_merge([t.data_ptr() for t in pb], r, 4096 + 12)
 torch.cuda.synchronize()
+ok &= all(np.array_equal(t.cpu().numpy(), want_or) for t in pb)
 o = OracleFilter(3, 1 << 20, B=256, S=64, k=8)
 o.add(keys)
 ok &= np.array_equal(outp.cpu().numpy().view(np.uint32), o.contains(q))
