@@ -64,7 +64,7 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="keys per rank (override)")
     ap.add_argument("--m-bits", dest="m_bits", type=int, default=None, help="filter bits (override)")
     ap.add_argument("--range-mib", type=int, default=0, help="binned add: filter MiB per range (0: library default)")
-    ap.add_argument("--merge", choices=["alltoall", "allgather", "nvls", "p2p"], default="alltoall")
+    ap.add_argument("--merge", choices=["alltoall", "allgather", "nvls", "p2p", "route"], default="alltoall")
     ap.add_argument("--add-mode", choices=["auto", "direct", "binned"], default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -262,16 +262,28 @@ def run_ours(a, cfg, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     words = f.data()
 
+    pf = None
+    if world > 1 and a.merge == "route":  # E3: route keys to block-range owners, gather the ranges
+        pf = bfdist.PartitionedFilter(cfg["m_bits"], cfg["k"], cfg["B"], cfg["S"], VARIANT_IDS[cfg["variant"]],
+                                      z=cfg["z"])
+
     def step(ev=None):
         if ev:
             ev[0].record(stream)
         f.clear()
+        if pf is not None:
+            pf.clear()
         if ev:
             ev[1].record(stream)
-        f.add(keys)
+        if pf is not None:
+            pf.add(keys)
+        else:
+            f.add(keys)
         if ev:
             ev[2].record(stream)
-        if world > 1:
+        if pf is not None:
+            pf.gather_into(words, cfg["B"] // 8)
+        elif world > 1:
             bfdist.MERGES[a.merge](words)
         if ev:
             ev[3].record(stream)

@@ -227,6 +227,17 @@ def build_replicated(filt, keys: torch.Tensor, strategy: str = "alltoall", group
     MERGES[strategy](filt.data(), group=group)
 
 
+def build_replicated_routed(pf, keys: torch.Tensor, words: torch.Tensor, block_bytes: int) -> None:
+    """E3: route every key to the owner of its block range
+    (hash once, all_to_all of records), each owner builds its range, then the
+    ranges are all-gathered into every rank's replica `words`.  Moves 8 B per
+    key plus (P-1)/P of the filter per rank, instead of E2's 2(P-1)/P of the
+    filter; no OR-fold (owners never overlap)."""
+    pf.clear()
+    pf.add(keys)
+    pf.gather_into(words, block_bytes)
+
+
 def lookup_sharded(filt, keys: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """Data-parallel lookup of this rank's shard against its replica (no
     communication)."""
@@ -269,6 +280,14 @@ class GpuRouteOps:
         out = torch.zeros((n + 31) // 32, dtype=torch.int32, device=idx.device)
         self.bf.bf_scatter_results(idx, res, counts, P, cap, out)
         return out
+
+    def part_bytes(self):
+        """This part's word array (a uint8 device view, no copy)."""
+        ptr, nbytes = self.bf.bf_data(self.h)
+        return self.bf._device_view(ptr, nbytes)
+
+    def clear(self):
+        self.bf.bf_clear(self.h)
 
 
 class PartitionedFilter:
@@ -321,6 +340,28 @@ class PartitionedFilter:
         recv = self._exchange(recs, P, cap)
         rcounts = self._exchange(counts, P, 1)
         self.ops.add_routed(recv, rcounts, P, cap)
+
+    def clear(self) -> None:
+        self.ops.clear()
+
+    def gather_into(self, words: torch.Tensor, block_bytes: int) -> None:
+        """E3's second half: all_gather every owner's block
+        range into `words`, the full filter's word array on every rank, so
+        that route-to-owner construction (``add``) yields a replica.  Parts
+        differ by at most one block; each rank sends its part padded to the
+        largest and the valid prefix of every part is copied to its offset
+        floor(p*b/P)*block_bytes."""
+        mine = self.ops.part_bytes()
+        P = self.P
+        b = words.numel() // block_bytes
+        offs = [b * p // P * block_bytes for p in range(P + 1)]
+        mx = max(offs[p + 1] - offs[p] for p in range(P))
+        send = torch.zeros(mx, dtype=torch.uint8, device=words.device)
+        send[:mine.numel()].copy_(mine)
+        recv = torch.empty(P * mx, dtype=torch.uint8, device=words.device)
+        dist.all_gather_into_tensor(recv, send, group=self.group)
+        for p in range(P):
+            words[offs[p]:offs[p + 1]].copy_(recv[p * mx:p * mx + offs[p + 1] - offs[p]])
 
     def contains(self, keys: torch.Tensor) -> torch.Tensor:
         self._dev = keys.device

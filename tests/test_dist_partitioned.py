@@ -68,6 +68,12 @@ class OracleRouteOps:
             res[slot] = int(self.bits[bits].all())
         return res
 
+    def part_bytes(self):
+        return torch.from_numpy(np.packbits(self.bits, bitorder="little"))
+
+    def clear(self):
+        self.bits[:] = 0
+
     def scatter(self, idx, res, counts, P, cap, n):
         out = np.zeros(n, dtype=np.uint8)
         for s in range(P):
@@ -106,7 +112,12 @@ def _worker(rank, world, port, m_bits, results):
         q = np.concatenate([mine[:700], synth.negatives(900, offset=rank * 1000)])
         got = pf.contains(torch.from_numpy(q.view(np.int64)))
         want = np.unpackbits(full.contains(q).view(np.uint8), bitorder="little")[: q.size]
-        results[rank] = (ok_bits, bool(np.array_equal(got, want)))
+        # E3: route-to-owner construction + all_gather of the parts = a replica
+        words = torch.zeros(full.nbytes, dtype=torch.uint8)
+        from paper_2512_15595_b200.dist import build_replicated_routed
+        build_replicated_routed(pf, torch.from_numpy(mine.view(np.int64)), words, 256 // 8)
+        ok_rep = bool(np.array_equal(words.numpy(), full.bytes()))
+        results[rank] = (ok_bits and ok_rep, bool(np.array_equal(got, want)))
     finally:
         dist.destroy_process_group()
 
