@@ -6,6 +6,8 @@ import subprocess
 
 import pytest
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 
 def test_library_exports_every_declared_symbol(bflib):
     declared = bflib.declared_symbols()
@@ -67,3 +69,38 @@ def test_instantiation_table_matches_generator(bflib):
     # every configs[1] sweep row has both default layouts compiled
     assert (1, 3, 256, 64, 8, 0, 1, 4, 4, 0) in inst  # contains SBF 256/64 k8 Θ1 Φ4 kpt4
     assert (0, 3, 256, 64, 8, 0, 4, 1, 1, 0) in inst  # add SBF 256/64 k8 Θ4 Φ1
+
+
+def _build_demo():
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if not gcc:
+        pytest.skip("no gcc")
+    from paper_2512_15595_b200 import build
+    build.build()
+    exe = os.path.join(ROOT, "examples", "bf_demo")
+    subprocess.check_call([gcc, "-O2", "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "bf_demo.c"), "-L", os.path.join(ROOT, "paper_2512_15595_b200"),
+                           "-lbf200", "-Wl,-rpath," + os.path.join(ROOT, "paper_2512_15595_b200"), "-o", exe])
+    return exe
+
+
+def test_c_demo_builds_against_the_header():
+    """include/bf.h is plain C99 and libbf200.so links into a C program with
+    no CUDA code of its own (examples/bf_demo.c)."""
+    import subprocess
+    exe = _build_demo()
+    r = subprocess.run([exe, "64"], capture_output=True, text=True)
+    import torch
+    if not torch.cuda.is_available():  # CPU box: a clean, reported failure
+        assert r.returncode == 1 and "bf_create failed: -3" in r.stderr
+
+
+@pytest.mark.gpu
+def test_c_demo_runs_on_gpu(cuda):
+    import subprocess
+    exe = _build_demo()
+    r = subprocess.run([exe, str(1 << 20)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "found 1048576/1048576" in r.stdout
