@@ -90,8 +90,10 @@ struct Cfg {
     // grid strides ahead with prefetch.global.L2 (one request per 128-byte
     // line, no registers): the key load at the top of a tile then waits for
     // L2 instead of HBM (+4-7% on SBF 256/64, kexp; no gain where keys are
-    // already register-prefetched or the block is staged in shared memory)
-    static constexpr int L2PF = BF_L2PF_DIST >= 0 ? BF_L2PF_DIST : ((THETA == 1 && !PREFETCH_T1 && !BBF_SM) ? 2 : 0);
+    // already register-prefetched or the block is staged in shared memory,
+    // -3..-5% on the Θ=1 layouts of 512/1024-bit blocks: profiles/r1_paper_tables.md)
+    static constexpr int L2PF =
+        BF_L2PF_DIST >= 0 ? BF_L2PF_DIST : ((THETA == 1 && !PREFETCH_T1 && !BBF_SM && B <= 256) ? 2 : 0);
     // BBF add (Θ > 1) with B >= 256: each lane ORs its own keys' whole
     // patterns into shared memory (one atomic per draw) and the group then
     // issues the coalesced REDs from there, instead of every lane of the group
