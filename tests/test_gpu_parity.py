@@ -94,6 +94,7 @@ GENERIC = [  # no specialized instantiation -> generic runtime kernel
     (3, 512, 32, 16, 0), (3, 1024, 32, 32, 0), (4, 1024, 32, 16, 4), (1, 512, 32, 20, 0),
     (3, 256, 64, 20, 0), (2, 64, 64, 25, 0), (4, 512, 32, 16, 8), (1, 32, 32, 3, 0),
     (3, 128, 32, 32, 0), (4, 256, 64, 8, 1),
+    (2, 32, 32, 1, 0), (1, 64, 64, 1, 0), (1, 1024, 64, 7, 0), (4, 1024, 32, 16, 16),  # k=1, 1024-bit BBF, z=16
 ]
 
 
@@ -700,3 +701,23 @@ def test_auto_add_path_threshold(bflib, cuda):
         o = OracleFilter(3, m, B=256, S=64, k=8, allocate=False)
         lo, hi = o.b // 2, o.b // 2 + 4096
         assert np.array_equal(_gpu_bytes(f)[lo * 32:hi * 32], o.add_range(synth.keys(5, n), lo, hi, threads=os.cpu_count()))
+
+
+@pytest.mark.parametrize("cfg,m", [((3, 256, 64, 8, 0), 1), ((3, 256, 64, 8, 0), 256), ((2, 32, 32, 4, 0), 32),
+                                   ((4, 256, 32, 8, 2), 100)])
+def test_single_block_filter(bflib, cuda, cfg, m):
+    """Degenerate geometry: b = ceil(m/B) = 1 (every key selects block 0; the
+    filter saturates), incl. m < B (m_eff = B, reading 11)."""
+    import torch
+    bf = bflib
+    v, B, S, k, z = cfg
+    keys = synth.keys(23, 777)
+    q = np.concatenate([keys[:100], synth.negatives(1000)])
+    o = OracleFilter(v, m, B=B, S=S, k=k, z=z)
+    o.add(keys)
+    f = bf.Filter(m, k, B, S, variant=v, z=z)
+    assert f.b == 1 and f.m_eff == B
+    f.add(_to_dev(torch, keys, cuda))
+    torch.cuda.synchronize()
+    assert np.array_equal(_gpu_bytes(f), o.bytes())
+    assert np.array_equal(_gpu_contains(torch, f, _to_dev(torch, q, cuda)), o.contains(q))
