@@ -41,10 +41,11 @@ struct Ctx {
 };
 
 template <class K>
-static float time_kernel(Ctx& c, K kern, const Params& p, int grid)
+static float time_kernel(Ctx& c, K kern, const Params& p, int grid, bool clear = false)
 {
     std::vector<float> ts;
     for (int r = 0; r < c.reps + 2; ++r) {
+        if (clear) CK(cudaMemset(c.words, 0, c.m_bits / 8));  // every add starts from an empty filter
         CK(cudaEventRecord(c.e0));
         kern<<<grid, 256>>>(p);
         CK(cudaEventRecord(c.e1));
@@ -78,7 +79,7 @@ static void run(Ctx& c, const char* name)
     // add timing (each rep re-adds the same keys: idempotent)
     CK(cudaMemset(c.words, 0, c.m_bits / 8));
     p.keys = c.keys;
-    float ta = time_kernel(c, bulk_kernel<CA, true>, p, occA * nsm);
+    float ta = time_kernel(c, bulk_kernel<CA, true>, p, occA * nsm, true);
     std::vector<unsigned char> fb(c.m_bits / 8);
     CK(cudaMemcpy(fb.data(), c.words, fb.size(), cudaMemcpyDeviceToHost));
     // contains on the positives
@@ -334,6 +335,38 @@ int main(int argc, char** argv)
     CK(cudaDeviceSynchronize());
     CK(cudaEventCreate(&c.e0));
     CK(cudaEventCreate(&c.e1));
+    if (argc > 1 && strcmp(argv[1], "ts") == 0) {
+        // dense (configs[1]: 4 bits/key) and iso-FPR-like (16 bits/key) loads
+        for (uint64_t nn : {c.n, c.n / 4}) {
+            const uint64_t keep = c.n;
+            c.n = nn;
+            run<Cfg<V_SBF, 64, 2, 8, 0, 4, 1, 4, 0>, Cfg<V_SBF, 64, 2, 8, 0, 1, 4, 4, 0>>(c, nn == keep ? "SBF256/64 k8 dense" : "SBF256/64 k8 16b/key");
+            run<Cfg<V_SBF, 32, 3, 8, 0, 8, 1, 4, 0>, Cfg<V_SBF, 32, 3, 8, 0, 1, 8, 4, 0>>(c, nn == keep ? "SBF256/32 k8 dense" : "SBF256/32 k8 16b/key");
+            run<Cfg<V_SBF, 64, 1, 16, 0, 2, 1, 4, 0>, Cfg<V_SBF, 64, 1, 16, 0, 1, 2, 4, 0>>(c, nn == keep ? "SBF128/64 k16 dense" : "SBF128/64 k16 16b/key");
+            run<Cfg<V_BBF, 64, 2, 8, 0, 4, 1, 2, 0>, Cfg<V_BBF, 64, 2, 8, 0, 1, 4, 4, 0>>(c, nn == keep ? "BBF256/64 k8 dense" : "BBF256/64 k8 16b/key");
+            run<Cfg<V_RBBF, 64, 0, 8, 0, 1, 1, 4, 0>, Cfg<V_RBBF, 64, 0, 8, 0, 1, 1, 4, 0>>(c, nn == keep ? "RBBF64 k8 dense" : "RBBF64 k8 16b/key");
+            c.n = keep;
+        }
+        return 0;
+    }
+    if (argc > 1 && strcmp(argv[1], "highk") == 0) {
+#define HK(V, S_, LGS, K, Z, NAME) run<Cfg<V, S_, LGS, K, Z, 1, (1 << LGS), 4, 0>, Cfg<V, S_, LGS, K, Z, 1, (1 << LGS), 4, 0>>(c, NAME)
+        HK(V_SBF, 64, 2, 8, 0, "SBF256/64 k8");
+        HK(V_SBF, 64, 2, 12, 0, "SBF256/64 k12");
+        HK(V_SBF, 64, 2, 16, 0, "SBF256/64 k16");
+        HK(V_SBF, 32, 3, 8, 0, "SBF256/32 k8");
+        HK(V_SBF, 32, 3, 16, 0, "SBF256/32 k16");
+        HK(V_CSBF, 32, 3, 8, 2, "CSBF256/32 z2 k8");
+        HK(V_CSBF, 32, 3, 12, 2, "CSBF256/32 z2 k12");
+        HK(V_CSBF, 32, 3, 16, 2, "CSBF256/32 z2 k16");
+        HK(V_CSBF, 32, 3, 16, 4, "CSBF256/32 z4 k16");
+        HK(V_CSBF, 64, 2, 12, 2, "CSBF256/64 z2 k12");
+        HK(V_CSBF, 64, 2, 16, 2, "CSBF256/64 z2 k16");
+        HK(V_SBF, 64, 1, 16, 0, "SBF128/64 k16");
+        HK(V_RBBF, 64, 0, 16, 0, "RBBF64 k16");
+#undef HK
+        return 0;
+    }
     if (argc > 1 && strcmp(argv[1], "bin") == 0) {
         using SBF8 = Cfg<V_SBF, 64, 2, 8, 0, 1, 4, 1, 0>;
         for (uint32_t kb : {128u, 64u}) {
