@@ -40,6 +40,9 @@
 #ifndef BF_L2PF_DIST
 #define BF_L2PF_DIST -1  // contains: prefetch keys this many tiles ahead into L2 (0 off, -1 rule)
 #endif
+#ifndef BF_KEY_SMEM
+#define BF_KEY_SMEM 1  // Θ=1 contains stages the key stream in shared memory (cp.async); 0 disables
+#endif
 #ifndef BF_T1_PIPE
 #define BF_T1_PIPE 0  // Θ=1 contains: two half-tiles of block loads in flight (software pipeline)
 #endif
@@ -92,6 +95,15 @@ struct Cfg {
     // L2 instead of HBM (+4-7% on SBF 256/64, kexp; no gain where keys are
     // already register-prefetched or the block is staged in shared memory,
     // -3..-5% on the Θ=1 layouts of 512/1024-bit blocks: profiles/r1_paper_tables.md)
+    // Θ=1 contains without the register key prefetch stages its key stream
+    // through shared memory with cp.async one tile ahead (contains_ksm):
+    // configs[1] SBF 256/64 k=8 228 -> 233, k=16 190 -> 215, CSBF 256/32 z=2
+    // k=16 165 -> 192 Gkeys/s (tools/kexp); where the register prefetch is
+    // on, staging is slower (RBBF 64 k=16 209 -> 167), and BBF blocks staged
+    // in shared memory gain from it only at k >= 12 (BBF 256/64 k=8 -7%,
+    // k=16 +7%: the two staging areas cost a CTA per SM)
+    static constexpr bool KEY_SMEM =
+        BF_KEY_SMEM && THETA == 1 && KPT % 2 == 0 && !PREFETCH_T1 && (!BBF_SM || K >= 12);
     static constexpr int L2PF =
         BF_L2PF_DIST >= 0 ? BF_L2PF_DIST : ((THETA == 1 && !PREFETCH_T1 && !BBF_SM && B <= 256) ? 2 : 0);
     // BBF add (Θ > 1) with B >= 256: each lane ORs its own keys' whole
@@ -465,7 +477,7 @@ __device__ __forceinline__ void load_tile_keys(const uint64_t* keys, uint64_t mi
 // registers (kin); the keys of this warp's next full tile are loaded into
 // knext while this tile's memory accesses are in flight (software pipeline:
 // the HBM latency of the key stream hides behind a whole tile of work).
-template <class C, bool ADD, bool FULL, bool USE_SM = true>
+template <class C, bool ADD, bool FULL, bool USE_SM = true, bool KIN = false>
 __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_t lane, uint32_t pos,
                                          uint32_t gbase, bool vec_ok, const SaltSrc<C>& ss,
                                          const uint64_t (&kin)[C::KPT], uint64_t (&knext)[C::KPT],
@@ -476,8 +488,8 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
     const uint64_t base = tile * (32 * KPT);
     const uint64_t mine = base + (uint64_t)lane * KPT;
 
-    // (1) ingest + hash once per key
-    constexpr bool PF = ADD || C::THETA > 1 || C::PREFETCH_T1;
+    // (1) ingest + hash once per key (KIN: the caller staged this tile's keys)
+    constexpr bool PF = ADD || C::THETA > 1 || C::PREFETCH_T1 || KIN;
     uint64_t key[KPT];
     bool valid[KPT];
     if constexpr (!PF) {
@@ -568,7 +580,7 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
         for (int j = 0; j < KPT; ++j) {
             if (FULL || valid[j]) load_block<C>((const W*)p.words, blk[j], wd[j]);
         }
-        if constexpr (C::PREFETCH_T1) {
+        if constexpr (C::PREFETCH_T1 && !KIN) {
             if (have_next) load_tile_keys<KPT>(p.keys, next_mine, vec_ok, knext);
         }
 #pragma unroll
@@ -621,6 +633,64 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
 
     // (3) coalesced write-back of the packed results
     if constexpr (!ADD) store_results<KPT>(p.out, tile, res, lane, (p.n + 31) / 32);
+}
+
+// Θ = 1 contains with the key stream staged through shared memory by
+// cp.async (LDGSTS, per lane, no registers held): the keys of tile t+1 are
+// copied while tile t is hashed, loaded and tested, so the hash at the top of
+// a tile starts from a shared-memory load instead of waiting for the key
+// stream (ncu: 20% of the warps' stall samples sat on the first IMAD of the
+// hash).  Double-buffered per warp: 2 x 32 x KPT keys.  Each lane reads only
+// the 32 bytes it copied itself, so cp.async.wait_group orders it (no
+// barrier).  Full tiles only; the ragged tail goes through run_tile.
+template <class C>
+__device__ __forceinline__ void contains_ksm(const Params& p, uint32_t* sm, uint64_t* kbuf, const uint32_t* s_salt,
+                                             const uint32_t* s_gsalt)
+{
+    constexpr int KPT = C::KPT;
+    static_assert(C::THETA == 1 && KPT % 2 == 0, "key staging: Θ = 1, 16-byte copies");
+    const uint32_t lane = threadIdx.x & 31u;
+    SaltSrc<C> ss;
+    ss.init(0, s_salt, s_gsalt);
+    constexpr uint64_t TILE = 32 * KPT;
+    const uint64_t ntiles = (p.n + TILE - 1) / TILE;
+    const uint64_t nfull = p.n / TILE;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint64_t* my = kbuf + lane * KPT;  // this lane's slot of buffer 0; buffer 1 at + 32*KPT
+    auto issue = [&](uint64_t t, int b) {
+        const uint64_t* src = p.keys + t * TILE + (uint64_t)lane * KPT;
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(my + b * 32 * KPT);
+#pragma unroll
+        for (int c = 0; c < KPT / 2; ++c)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * c), "l"(src + 2 * c) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int b = 0;
+    if (gw < nfull) issue(gw, 0);
+    for (uint64_t t = gw; t < nfull; t += nw) {
+        const uint64_t tn = t + nw;
+        if (tn < nfull) {
+            issue(tn, b ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        uint64_t kin[KPT], knext[KPT];
+        const uint64_t* kb = my + b * 32 * KPT;
+#pragma unroll
+        for (int j = 0; j < KPT; j += 2) {
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(kb + j);
+            kin[j] = v.x;
+            kin[j + 1] = v.y;
+        }
+        run_tile<C, false, true, true, true>(p, t, lane, 0, 0, true, ss, kin, knext, false, 0, sm);
+        b ^= 1;
+    }
+    if (ntiles > nfull && gw == nfull % nw) {
+        uint64_t kin[KPT] = {}, knext[KPT];
+        run_tile<C, false, false>(p, nfull, lane, 0, 0, true, ss, kin, knext, false, 0, sm);
+    }
 }
 
 // Θ = 1 contains, software-pipelined over half tiles.  A lane's KPT keys
@@ -725,6 +795,13 @@ __global__ void __launch_bounds__(256) bulk_kernel(const Params p)
     if constexpr (!ADD && BF_T1_PIPE && C::THETA == 1 && C::KPT >= 2 && C::HS == 0 && C::HV == 0) {
         contains_pipe<C>(p, sm);
         return;
+    }
+    if constexpr (!ADD && C::KEY_SMEM) {
+        __shared__ __align__(16) uint64_t s_keys[8 * 2 * 32 * C::KPT];
+        if ((((uintptr_t)p.keys) & 15) == 0) {  // 16-byte cp.async; else the plain tile loop
+            contains_ksm<C>(p, sm, s_keys + (threadIdx.x >> 5) * (2 * 32 * C::KPT), s_salt, s_gsalt);
+            return;
+        }
     }
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t pos = lane & (uint32_t)(C::THETA - 1);
