@@ -335,6 +335,16 @@ int main(int argc, char** argv)
     CK(cudaDeviceSynchronize());
     CK(cudaEventCreate(&c.e0));
     CK(cudaEventCreate(&c.e1));
+    if (argc > 1 && strcmp(argv[1], "csbf") == 0) {
+        run<Cfg<V_CSBF, 32, 3, 8, 2, 2, 4, 4, 0>, Cfg<V_CSBF, 32, 3, 8, 2, 1, 8, 4, 0>>(c, "CSBF256/32 z2 k8");
+        run<Cfg<V_CSBF, 32, 3, 16, 2, 2, 4, 4, 0>, Cfg<V_CSBF, 32, 3, 16, 2, 1, 8, 4, 0>>(c, "CSBF256/32 z2 k16");
+        run<Cfg<V_CSBF, 32, 3, 8, 4, 4, 2, 4, 0>, Cfg<V_CSBF, 32, 3, 8, 4, 1, 8, 4, 0>>(c, "CSBF256/32 z4 k8");
+        run<Cfg<V_CSBF, 64, 2, 8, 2, 2, 2, 4, 0>, Cfg<V_CSBF, 64, 2, 8, 2, 1, 4, 4, 0>>(c, "CSBF256/64 z2 k8");
+        run<Cfg<V_CSBF, 64, 2, 16, 2, 2, 2, 4, 0>, Cfg<V_CSBF, 64, 2, 16, 2, 1, 4, 4, 0>>(c, "CSBF256/64 z2 k16");
+        run<Cfg<V_BBF, 64, 1, 8, 0, 2, 1, 4, 0>, Cfg<V_BBF, 64, 1, 8, 0, 1, 2, 4, 0>>(c, "BBF128/64 k8");
+        run<Cfg<V_BBF, 64, 1, 16, 0, 2, 1, 4, 0>, Cfg<V_BBF, 64, 1, 16, 0, 1, 2, 4, 0>>(c, "BBF128/64 k16");
+        return 0;
+    }
     if (argc > 1 && strcmp(argv[1], "ts") == 0) {
         // dense (configs[1]: 4 bits/key) and iso-FPR-like (16 bits/key) loads
         for (uint64_t nn : {c.n, c.n / 4}) {
