@@ -335,6 +335,19 @@ int main(int argc, char** argv)
     CK(cudaDeviceSynchronize());
     CK(cudaEventCreate(&c.e0));
     CK(cudaEventCreate(&c.e1));
+    if (argc > 1 && strcmp(argv[1], "pipe") == 0) {
+#define PK(V, S_, LGS, K, Z, KP, NAME) run<Cfg<V, S_, LGS, K, Z, (1 << LGS), 1, 4, 0>, Cfg<V, S_, LGS, K, Z, 1, (1 << LGS), KP, 0>>(c, NAME)
+        PK(V_SBF, 64, 2, 8, 0, 4, "SBF256/64 k8 kpt4");
+        PK(V_SBF, 64, 2, 8, 0, 2, "SBF256/64 k8 kpt2");
+        PK(V_SBF, 64, 2, 16, 0, 4, "SBF256/64 k16 kpt4");
+        PK(V_SBF, 64, 2, 16, 0, 2, "SBF256/64 k16 kpt2");
+        PK(V_SBF, 32, 3, 16, 0, 4, "SBF256/32 k16 kpt4");
+        PK(V_SBF, 32, 3, 16, 0, 2, "SBF256/32 k16 kpt2");
+        PK(V_CSBF, 32, 3, 16, 2, 4, "CSBF256/32 z2 k16 kpt4");
+        PK(V_CSBF, 32, 3, 16, 2, 2, "CSBF256/32 z2 k16 kpt2");
+#undef PK
+        return 0;
+    }
     if (argc > 1 && strcmp(argv[1], "csbf") == 0) {
         run<Cfg<V_CSBF, 32, 3, 8, 2, 2, 4, 4, 0>, Cfg<V_CSBF, 32, 3, 8, 2, 1, 8, 4, 0>>(c, "CSBF256/32 z2 k8");
         run<Cfg<V_CSBF, 32, 3, 16, 2, 2, 4, 4, 0>, Cfg<V_CSBF, 32, 3, 16, 2, 1, 8, 4, 0>>(c, "CSBF256/32 z2 k16");
