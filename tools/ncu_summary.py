@@ -53,6 +53,10 @@ def launches(path):
 
 PER_KEY = [  # (metric, label, multiplier): per-key evidence (SURVEY 8(d) "ncu evidence per design choice")
     ("smsp__inst_executed.sum", "thread instructions / key", 32),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "L1 global-load requests (warp instructions) / key", 1),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "L1 global-load sectors / key", 1),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_red.sum", "L1 RED requests (warp instructions) / key", 1),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum", "L1 RED sectors / key", 1),
     ("lts__t_requests_srcunit_tex_op_read.sum", "L2 read requests / key", 1),
     ("lts__t_requests_srcunit_tex_op_red.sum", "L2 RED requests / key (1.0 = Θ lanes coalesced into one request)", 1),
     ("lts__t_sectors_srcunit_tex_op_red.sum", "L2 RED sectors / key", 1),
