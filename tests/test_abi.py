@@ -104,3 +104,56 @@ def test_c_demo_runs_on_gpu(cuda):
     r = subprocess.run([exe, str(1 << 20)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert "found 1048576/1048576" in r.stdout
+
+
+# SURVEY 8(b) validation rules (include/bf.h): checked before any CUDA call,
+# so they hold on the CPU box too.
+_INVALID_CREATE = [
+    (1 << 20, 8, 256, 16, 3),        # word_bits not 32/64
+    (1 << 20, 8, 96, 32, 3),         # block_bits not a power of two
+    (1 << 20, 8, 2048, 64, 3),       # block_bits > 1024
+    (1 << 20, 8, 32, 64, 3),         # block_bits < word_bits
+    (1 << 20, 0, 256, 64, 3),        # k < 1
+    (1 << 20, 33, 256, 64, 3),       # k > 32
+    (1 << 20, 8, 256, 64, 2),        # RBBF needs B == S
+    (1 << 20, 6, 256, 64, 3),        # SBF needs k % s == 0
+    (1 << 20, 8, 256, 32, 4 | (3 << 8)),  # CSBF z must divide s
+    (1 << 20, 9, 256, 32, 4 | (2 << 8)),  # CSBF z must divide k
+    (0, 8, 256, 64, 3),              # m_bits >= 1
+    ((1 << 32) * 256 + 1, 8, 256, 64, 3),  # b > 2^32
+    (1 << 20, 8, 256, 64, 9),        # unknown variant
+    (1 << 20, 8, 256, 64, 3 | (2 << 8)),  # z only for CSBF
+    (1 << 20, 8, 256, 64, 3 | (3 << 16)),  # unknown draw scheme
+    ((1 << 32) + 1, 8, 0, 0, 0),     # CBF needs m <= 2^32
+]
+
+
+@pytest.mark.parametrize("args", _INVALID_CREATE)
+def test_create_rejects_invalid_configs(bflib, args):
+    with pytest.raises(bflib.BFError) as ei:
+        bflib.bf_create(*args)
+    assert ei.value.code == bflib.BF_EINVAL, ei.value
+
+
+def test_create_valid_config_reaches_the_device(bflib):
+    """A valid configuration passes validation; without a GPU the failure is
+    the device's (BF_ECUDA), never a validation error."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: creation succeeds (tests/test_gpu_parity.py)")
+    for args in [(1 << 20, 8, 256, 64, 3), (1 << 20, 8, 256, 32, 4 | (2 << 8)), (1 << 20, 7, 0, 0, 0),
+                 (1 << 20, 16, 1024, 64, 1), ((1 << 32) * 256, 8, 256, 64, 3)]:
+        with pytest.raises(bflib.BFError) as ei:
+            bflib.bf_create(*args)
+        assert ei.value.code == bflib.BF_ECUDA, (args, ei.value)
+
+
+def test_null_handle_calls_fail_cleanly(bflib):
+    import ctypes
+    L = ctypes.CDLL(bflib.LIB_PATH)
+    L.bf_add.restype = ctypes.c_int
+    L.bf_add.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
+    assert L.bf_add(None, None, 10, None) == bflib.BF_EINVAL
+    L.bf_destroy.argtypes = [ctypes.c_void_p]
+    L.bf_destroy(None)  # NULL-safe
+    assert bflib.last_error()[0] in (bflib.BF_EINVAL, bflib.BF_OK)
