@@ -147,15 +147,19 @@ def test_sizes_and_tails(bflib, cuda, cfg, n):
 
 
 @pytest.mark.parametrize("cfg", EDGE_CFGS)
-def test_unaligned_keys_idempotence_clear_seed(bflib, cuda, cfg):
+@pytest.mark.parametrize("off", [1, 2])
+def test_unaligned_keys_idempotence_clear_seed(bflib, cuda, cfg, off):
+    """Key arrays 8-byte aligned (off=1: scalar key loads, no cp.async key
+    staging) and 16- but not 32-byte aligned (off=2: staging on, the 256-bit
+    key loads off) give the oracle's bits, for several seeds and layouts."""
     import torch
     bf = bflib
     v, B, S, k, z = cfg
     m = 1 << 18
     keys = synth.keys(3, 10001)
-    buf = _to_dev(torch, np.concatenate([np.zeros(1, np.uint64), keys]), cuda)
-    kd = buf[1:]  # 8-byte aligned, not 16/32-byte aligned
-    assert kd.data_ptr() % 32 != 0
+    buf = _to_dev(torch, np.concatenate([np.zeros(off, np.uint64), keys]), cuda)
+    kd = buf[off:]
+    assert kd.data_ptr() % 32 != 0 and kd.data_ptr() % 16 == (0 if off == 2 else 8)
     for seed in (0, 1, 0xDEADBEEF):
         o = OracleFilter(v, m, B=B, S=S, k=k, z=z, seed=seed)
         o.add(keys)
@@ -172,8 +176,8 @@ def test_unaligned_keys_idempotence_clear_seed(bflib, cuda, cfg):
             torch.cuda.synchronize()
             assert np.array_equal(_gpu_bytes(f), o.bytes())
             q = np.concatenate([keys[:999], synth.negatives(1001)])
-            qbuf = _to_dev(torch, np.concatenate([np.zeros(1, np.uint64), q]), cuda)
-            assert np.array_equal(_gpu_contains(torch, f, qbuf[1:]), o.contains(q))
+            qbuf = _to_dev(torch, np.concatenate([np.zeros(off, np.uint64), q]), cuda)
+            assert np.array_equal(_gpu_contains(torch, f, qbuf[off:]), o.contains(q))
         f.clear()
         torch.cuda.synchronize()
         assert not _gpu_bytes(f).any()
