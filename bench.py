@@ -393,7 +393,8 @@ def run_ours(a, cfg, rank, world, local_rank):
         hit = [v for k, v in tr["kernels"].items() if any(sg in k for sg in sigs) and v.get("n") == n]
         if hit:
             roofline["traffic"] = hit[0]["dram_bytes_per_launch"]
-            roofline["traffic_source"] = tr.get("source")
+            roofline["traffic_source"] = (f"ncu --set full capture {hit[0].get('capture')} "
+                                          "(dram__bytes_read.sum + dram__bytes_write.sum per launch)")
     except Exception:
         pass
     if probe:

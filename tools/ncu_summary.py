@@ -118,9 +118,10 @@ def traffic(path, n_keys, out_json):
             float(r[h.index("dram__bytes_write.sum")].replace(",", "")) * scale[rows[1][h.index("dram__bytes_write.sum")]]
         acc[r[h.index("Kernel Name")]].append(b)
     old = json.load(open(out_json)) if os.path.exists(out_json) else {"kernels": {}}
-    old["source"] = f"ncu --set full capture {os.path.basename(path)} (dram__bytes_read.sum + dram__bytes_write.sum per launch)"
+    old["source"] = "ncu --set full captures (dram__bytes_read.sum + dram__bytes_write.sum per launch), one entry per kernel and key count"
     for k, v in acc.items():
-        old["kernels"][k] = {"dram_bytes_per_launch": sum(v) / len(v), "n": int(n_keys), "capture": os.path.basename(path)}
+        old["kernels"][f"{k} [n={int(n_keys)}]"] = {"dram_bytes_per_launch": sum(v) / len(v), "n": int(n_keys),
+                                                    "capture": os.path.basename(path)}
     json.dump(old, open(out_json, "w"), indent=1)
 
 
