@@ -335,6 +335,15 @@ int main(int argc, char** argv)
     CK(cudaDeviceSynchronize());
     CK(cudaEventCreate(&c.e0));
     CK(cudaEventCreate(&c.e1));
+    if (argc > 1 && strcmp(argv[1], "bbfadd") == 0) {
+        run<Cfg<V_BBF, 64, 2, 8, 0, 4, 1, 2, 0>, Cfg<V_BBF, 64, 2, 8, 0, 1, 4, 4, 0>>(c, "BBF256/64 k8");
+        run<Cfg<V_BBF, 64, 2, 12, 0, 4, 1, 2, 0>, Cfg<V_BBF, 64, 2, 12, 0, 1, 4, 4, 0>>(c, "BBF256/64 k12");
+        run<Cfg<V_BBF, 64, 2, 16, 0, 4, 1, 2, 0>, Cfg<V_BBF, 64, 2, 16, 0, 1, 4, 4, 0>>(c, "BBF256/64 k16");
+        run<Cfg<V_BBF, 64, 2, 16, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 16, 0, 1, 4, 4, 0>>(c, "BBF256/64 k16 kpt4");
+        run<Cfg<V_BBF, 32, 3, 8, 0, 8, 1, 4, 0>, Cfg<V_BBF, 32, 3, 8, 0, 1, 8, 4, 0>>(c, "BBF256/32 k8");
+        run<Cfg<V_BBF, 32, 3, 11, 0, 8, 1, 2, 0>, Cfg<V_BBF, 32, 3, 11, 0, 1, 8, 4, 0>>(c, "BBF256/32 k11");
+        return 0;
+    }
     if (argc > 1 && strcmp(argv[1], "pipe") == 0) {
 #define PK(V, S_, LGS, K, Z, KP, NAME) run<Cfg<V, S_, LGS, K, Z, (1 << LGS), 1, 4, 0>, Cfg<V, S_, LGS, K, Z, 1, (1 << LGS), KP, 0>>(c, NAME)
         PK(V_SBF, 64, 2, 8, 0, 4, "SBF256/64 k8 kpt4");
