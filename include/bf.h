@@ -37,8 +37,10 @@ extern "C" {
 
 /* Filter variants; numbering follows S:L272.
  *   BF_CBF  classical Bloom filter: k positions anywhere in
- *           m <= 2^32 bits (block_bits / word_bits are ignored; storage is
+ *           m <= 2^38 bits (block_bits / word_bits are ignored; storage is
  *           32-bit words).  The paper's GPU baseline.
+ *           Position j = fast range of d_j = h * C_j mod 2^64 onto [0, m):
+ *           ((d_j >> 32) * m) >> 32 for m <= 2^32, (d_j * m) >> 64 above.
  *   BF_BBF  blocked: all k bits inside one B-bit block.
  *   BF_RBBF register-blocked: B == S, one word per key.
  *   BF_SBF  sectorized: block = s = B/S words, k/s bits per word.

@@ -133,9 +133,12 @@ static const uint32_t GSALT[16] = {
 const uint32_t* bfo_salt_table(void) { return SALT; }
 const uint32_t* bfo_gsalt_table(void) { return GSALT; }
 
-/* CBF (oracle-only, used to check Eq. 1): k global positions from
- * 64-bit multiply-shift with odd 64-bit constants C_j = mix64(0xCBF + j) | 1.
- * See DESIGN.md "Readings" item CBF. */
+/* CBF (the paper's GPU baseline): k global
+ * positions from 64-bit multiply-shift with odd 64-bit constants
+ * C_j = mix64(0xCBF + j) | 1: d_j = h * C_j mod 2^64, then the fast range of
+ * d_j onto [0, m) -- ((d_j >> 32) * m) >> 32 for m <= 2^32 and the full
+ * (d_j * m) >> 64 (128-bit product) for larger m (up to 2^38 bits).  See
+ * DESIGN.md "Readings" item CBF. */
 static uint64_t mix64_const(uint64_t x)
 {
     uint64_t z = x + 0x9E3779B97F4A7C15ULL;
@@ -158,7 +161,7 @@ int bfo_validate(int variant, uint64_t m_bits, uint32_t B, uint32_t S,
                  uint32_t k, uint32_t z)
 {
     if (m_bits < 1 || k < 1 || k > 32) return BFO_EINVAL;
-    if (variant == BFO_CBF) return m_bits <= (1ULL << 32) ? BFO_OK : BFO_EINVAL;
+    if (variant == BFO_CBF) return m_bits <= (1ULL << 38) ? BFO_OK : BFO_EINVAL;
     if (S != 32 && S != 64) return BFO_EINVAL;
     if (!is_pow2(B) || B < S || B > 1024) return BFO_EINVAL;
     uint32_t s = B / S;
@@ -262,7 +265,10 @@ void bfo_pattern(const bfo_filter* f, uint64_t key, uint64_t* block, uint64_t* p
         for (uint32_t j = 0; j < f->k; ++j) {
             uint64_t c = mix64_const(0xCBFULL + j) | 1ULL;
             uint64_t d = h * c;
-            pos[j] = ((d >> 32) * f->m_bits) >> 32;
+            if (f->m_bits <= (1ULL << 32))
+                pos[j] = ((d >> 32) * f->m_bits) >> 32;
+            else
+                pos[j] = (uint64_t)(((unsigned __int128)d * f->m_bits) >> 64);
         }
         return;
     }

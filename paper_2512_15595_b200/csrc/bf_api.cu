@@ -160,10 +160,10 @@ struct bf_filter {
 static int validate(uint64_t m_bits, uint32_t k, uint32_t B, uint32_t S, uint32_t variant, uint32_t* z_out)
 {
     const uint32_t v = variant & 0xFF, z = (variant >> 8) & 0xFF;
-    if (v == BF_CBF) {  // classical filter: k positions over m <= 2^32 bits
+    if (v == BF_CBF) {  // classical filter: k positions over m <= 2^38 bits
         if (variant >> 8) return fail(BF_EINVAL, "unknown variant bits 0x%x", variant);
         if (k < 1 || k > 32) return fail(BF_EINVAL, "k must be in 1..32 (got %u)", k);
-        if (m_bits < 1 || m_bits > (1ULL << 32)) return fail(BF_EINVAL, "CBF needs 1 <= m_bits <= 2^32");
+        if (m_bits < 1 || m_bits > (1ULL << 38)) return fail(BF_EINVAL, "CBF needs 1 <= m_bits <= 2^38");
         *z_out = 0;
         return BF_OK;
     }

@@ -1,9 +1,11 @@
 // bf_cbf.cu -- the classical Bloom filter on the GPU (NEXT N3): the paper's
 // GPU CBF baseline ("1.45 and 8.84 billion operations per
 // second", "13.43 ... 42.64").  k positions anywhere in the m-bit array
-// (m <= 2^32), one red.global.or.b32 per position on add, one 32-bit load per
+// (m <= 2^38), one red.global.or.b32 per position on add, one 32-bit load per
 // position on contains.  Pattern (CBF reading):
-//   p_j = (((h * C_j) mod 2^64) >> 32) * m >> 32,  C_j = mix64(0xCBF + j) | 1
+//   d_j = (h * C_j) mod 2^64,  C_j = mix64(0xCBF + j) | 1
+//   p_j = (d_j >> 32) * m >> 32          for m <= 2^32
+//   p_j = hi64(d_j * m)  (__umul64hi)    for m >  2^32 (the 1 GB baseline)
 // Storage: bit p = bit p%32 of 32-bit word p/32 (= bit p%8 of byte p/8, LE).
 #include <cuda_runtime.h>
 
@@ -21,6 +23,11 @@ static __constant__ uint64_t c_cbf[32] = {
 #undef C
 };
 
+__device__ __forceinline__ uint64_t cbf_pos(uint64_t d, uint64_t m)
+{
+    return m <= (1ULL << 32) ? ((d >> 32) * m) >> 32 : __umul64hi(d, m);
+}
+
 template <bool ADD, int K>
 __global__ void __launch_bounds__(256) cbf_kernel(const Params p)
 {
@@ -36,14 +43,14 @@ __global__ void __launch_bounds__(256) cbf_kernel(const Params p)
             if (ADD) {
 #pragma unroll
                 for (int j = 0; j < K; ++j) {
-                    const uint64_t pos = (((h * c_cbf[j]) >> 32) * m) >> 32;
+                    const uint64_t pos = cbf_pos(h * c_cbf[j], m);
                     red_or(F + (pos >> 5), 1u << (pos & 31));
                 }
             } else {
                 uint32_t acc = 1;
 #pragma unroll
                 for (int j = 0; j < K; ++j) {  // all K loads in flight
-                    const uint64_t pos = (((h * c_cbf[j]) >> 32) * m) >> 32;
+                    const uint64_t pos = cbf_pos(h * c_cbf[j], m);
                     acc &= __ldg(F + (pos >> 5)) >> (pos & 31);
                 }
                 ok = acc & 1u;

@@ -124,7 +124,7 @@ _INVALID_CREATE = [
     (1 << 20, 8, 256, 64, 9),        # unknown variant
     (1 << 20, 8, 256, 64, 3 | (2 << 8)),  # z only for CSBF
     (1 << 20, 8, 256, 64, 3 | (3 << 16)),  # unknown draw scheme
-    ((1 << 32) + 1, 8, 0, 0, 0),     # CBF needs m <= 2^32
+    ((1 << 38) + 1, 8, 0, 0, 0),     # CBF needs m <= 2^38
 ]
 
 

@@ -452,10 +452,12 @@ def test_iso_fpr_configs1_rows(bflib, cuda, row):
     assert got.all()
 
 
-@pytest.mark.parametrize("m,k", [(1 << 20, 7), ((1 << 22) + 13, 16), (1 << 25, 16), (999_983, 1), (1 << 32, 4)])
+@pytest.mark.parametrize("m,k", [(1 << 20, 7), ((1 << 22) + 13, 16), (1 << 25, 16), (999_983, 1), (1 << 32, 4),
+                                 ((1 << 33) + 7, 16)])
 def test_cbf_matches_oracle(bflib, cuda, m, k):
     """GPU classical Bloom filter (NEXT N3; the paper's GPU CBF baseline,
-    P:L352/P:L392) == the oracle's CBF, bits and results, incl. m = 2^32."""
+    P:L352/P:L392) == the oracle's CBF, bits and results, incl. m = 2^32 and
+    the 128-bit fast range above it (m = 2^33 + 7, the 1 GB baseline)."""
     import torch
     bf = bflib
     keys = synth.keys(5, 70_001)

@@ -153,3 +153,35 @@ def test_draw_schemes_fpr_matches_exact_model(scheme, cfg):
     h = OracleFilter(v, m, B=B, S=S, k=k, z=z, scheme=scheme)
     h.add(synth.positives(n)[:1000])
     assert not np.array_equal(g.bytes(), h.bytes())
+
+
+def test_cbf_large_m_positions():
+    """CBF above 2^32 bits (the paper's 1 GB baseline): positions are
+    the 128-bit fast range (d_j * m) >> 64 of d_j = h * C_j mod 2^64.
+    Pinned by (i) the power-of-two special case, where the fast range is
+    exactly the top log2(m) bits of d_j (h from the xxhash library, C_j from
+    the stated constant rule), (ii) boundedness and uniformity over a
+    non-power-of-two m (chi-square over 64 equal cells), and (iii) m <= 2^32
+    keeping the 32-bit form (the existing CBF pins)."""
+    import xxhash
+    from scipy import stats
+    k = 16
+    m2 = 1 << 33
+    g = OracleFilter(CBF, m2, k=k, allocate=False)
+    C = [(int(synth.mix64(np.uint64(0xCBF + j))) | 1) for j in range(k)]
+    for key in synth.keys(99, 300):
+        h = xxhash.xxh64_intdigest(int(key).to_bytes(8, "little"), 0)
+        _, pos = g.pattern(int(key))
+        assert pos == [((h * c) % (1 << 64)) >> (64 - 33) for c in C]
+    m = (1 << 33) + 12345
+    g = OracleFilter(CBF, m, k=k, allocate=False)
+    cells = np.zeros(64, np.int64)
+    for key in synth.keys(7, 20_000):
+        _, pos = g.pattern(int(key))
+        assert max(pos) < m
+        for p in pos:
+            cells[p * 64 // m] += 1
+    assert stats.chisquare(cells).pvalue > 1e-4
+    assert any(p >= (1 << 32) for p in pos)  # the range above 2^32 is reached
+    with pytest.raises(ValueError):
+        OracleFilter(CBF, (1 << 38) + 1, k=k, allocate=False)
