@@ -50,7 +50,7 @@ def test_validation_without_gpu(bflib):
         bf.bf_create(1 << 20, 6, 256, 32, bf.BF_CSBF_Z(4))  # k % z != 0
     assert e.value.code == bf.BF_EINVAL
     with pytest.raises(bf.BFError) as e:
-        bf.bf_create((1 << 32) + 1, 8, 256, 64, bf.BF_CBF)  # CBF positions need m <= 2^32
+        bf.bf_create((1 << 38) + 1, 8, 256, 64, bf.BF_CBF)  # CBF positions need m <= 2^38
     assert e.value.code == bf.BF_EINVAL
     with pytest.raises(bf.BFError) as e:
         bf.bf_create(1 << 20, 0, 256, 64, bf.BF_BBF)
