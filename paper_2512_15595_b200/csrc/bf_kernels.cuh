@@ -18,9 +18,16 @@
 // into one L2 request per sector.  contains combines the
 // group's verdict with one ballot.
 //
-// Results (contains) stay in registers until the tile is done, then one
-// ballot per key slot packs them and KPT lanes store KPT consecutive words
-// (P:L245 step (3) "written back in a coalesced fashion").
+// Results (contains) stay in registers until the tile is done, then a
+// shift and log2(32/KPT) shuffle-xor steps pack them and KPT lanes store KPT
+// consecutive words (P:L245 step (3) "written back in a coalesced fashion").
+//
+// Key stream: add and cooperative contains load the next tile's keys into
+// registers while the current tile's accesses are in flight; Θ=1 contains
+// either does the same (small blocks) or, when the blocks leave no registers
+// for it, stages the next tile's keys in shared memory with per-lane
+// cp.async (contains_ksm).  Keys are read with evict_first so the stream
+// does not push the filter out of L2.
 //
 // The salts are compile-time immediates whenever the word index is
 // compile-time (Θ = 1), per-thread registers loaded once per kernel when the
