@@ -727,3 +727,32 @@ def test_single_block_filter(bflib, cuda, cfg, m):
     torch.cuda.synchronize()
     assert np.array_equal(_gpu_bytes(f), o.bytes())
     assert np.array_equal(_gpu_contains(torch, f, _to_dev(torch, q, cuda)), o.contains(q))
+
+
+def test_autotune_picks_a_compiled_schedule_and_keeps_results(bflib, cuda):
+    """paper_2512_15595_b200.tune.autotune (the paper's layout grid search at
+    run time): the chosen schedule is one of the compiled ones, contains
+    tuning leaves the filter untouched, add tuning leaves it empty, and the
+    tuned filter still equals the oracle's."""
+    import torch
+    from paper_2512_15595_b200 import tune
+    bf = bflib
+    m, n = 1 << 24, 50_000
+    keys = synth.keys(41, n)
+    o = OracleFilter(4, m, B=256, S=32, k=8, z=2)
+    o.add(keys)
+    f = bf.Filter(m, 8, 256, 32, "CSBF", z=2)
+    with pytest.raises(ValueError):
+        tune.autotune(f, 0, n=1 << 16)
+    r0 = tune.autotune(f, 0, n=1 << 18, reps=2, allow_clear=True)
+    assert len(r0["tried"]) >= 2 and r0["layout"] in r0["tried"]
+    assert (f.layout(0)["theta"], f.layout(0)["phi"], f.layout(0)["kpt"]) == r0["layout"]
+    assert not _gpu_bytes(f).any()
+    f.add(_to_dev(torch, keys, cuda))
+    torch.cuda.synchronize()
+    before = _gpu_bytes(f).copy()
+    r1 = tune.autotune(f, 1, n=1 << 18, reps=2)
+    assert r1["layout"] in r1["tried"] and np.array_equal(_gpu_bytes(f), before)
+    assert np.array_equal(before, o.bytes())
+    q = np.concatenate([keys[:999], synth.negatives(5000)])
+    assert np.array_equal(_gpu_contains(torch, f, _to_dev(torch, q, cuda)), o.contains(q))
