@@ -107,9 +107,6 @@ __device__ __forceinline__ void rotl64c(uint32_t& lo, uint32_t& hi)
 //   h ^= h >> 33;  h *= P2;  h ^= h >> 29;  h *= P3;  h ^= h >> 32
 __device__ __forceinline__ uint64_t xxh64_u64(uint64_t key, uint64_t seed)
 {
-#ifdef BF_DIAG_NOHASH  // diagnostic only (tools/kexp): keys are already uniform
-    return key ^ seed;
-#endif
     const uint64_t h0 = seed + XXP5 + 8ULL;
     uint32_t lo = (uint32_t)key, hi = (uint32_t)(key >> 32);
     mul64c<XXP2>(lo, hi);
@@ -179,11 +176,6 @@ __device__ __forceinline__ unsigned long long shl_clamp(unsigned long long v, ui
 // marks them evict-first in L2; ptxas accepts .L2::evict_first only there).
 __device__ __forceinline__ void ld_keys4(const uint64_t* p, uint64_t (&k)[4])
 {
-#ifdef BF_KEY_L1
-    asm("ld.global.nc.L1::evict_first.L2::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
-                 : "=l"(k[0]), "=l"(k[1]), "=l"(k[2]), "=l"(k[3]) : "l"(p));
-    return;
-#endif
     asm("ld.global.nc.L1::no_allocate.L2::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
                  : "=l"(k[0]), "=l"(k[1]), "=l"(k[2]), "=l"(k[3]) : "l"(p));
 }

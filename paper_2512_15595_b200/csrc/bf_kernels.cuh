@@ -50,12 +50,6 @@
 #ifndef BF_KEY_SMEM
 #define BF_KEY_SMEM 1  // Θ=1 contains stages the key stream in shared memory (cp.async); 0 disables
 #endif
-#ifndef BF_T1_PIPE
-#define BF_T1_PIPE 0  // Θ=1 contains: two half-tiles of block loads in flight (software pipeline)
-#endif
-#ifndef BF_L1PF_DIST
-#define BF_L1PF_DIST 0  // contains: prefetch the key tile this many tiles ahead into L1 (0: off)
-#endif
 
 namespace bf {
 
@@ -466,10 +460,6 @@ template <int KPT>
 __device__ __forceinline__ void load_tile_keys(const uint64_t* keys, uint64_t mine, bool vec_ok,
                                                uint64_t (&key)[KPT])
 {
-#ifdef BF_DIAG_SYNTHKEYS  // diagnostic only (tools/kexp): keys made in registers, no key stream
-    for (int j = 0; j < KPT; ++j) key[j] = mix64(mine + j);
-    return;
-#endif
     if (vec_ok) {
         if constexpr (KPT == 4) ld_keys4(keys + mine, key);
         else if constexpr (KPT == 2) ld_keys2(keys + mine, key);
@@ -700,88 +690,6 @@ __device__ __forceinline__ void contains_ksm(const Params& p, uint32_t* sm, uint
     }
 }
 
-// Θ = 1 contains, software-pipelined over half tiles.  A lane's KPT keys
-// of a tile are split into halves A (keys 0..H-1) and B (H..KPT-1); the loads
-// of one half are always in flight while the other half is tested:
-//   issue B(t) | load keys(t+1) | test A(t) | issue A(t+1) | test B(t) | store
-// so a warp never waits with nothing in flight (the plain tile loop issues
-// all KPT loads, then idles until they return).  Full tiles only; the ragged
-// tail goes through run_tile.  Same bits as every other schedule.
-template <class C>
-__device__ __forceinline__ void contains_pipe(const Params& p, uint32_t* sm)
-{
-    using W = typename C::W;
-    constexpr int KPT = C::KPT, H = KPT / 2;
-    static_assert(C::THETA == 1 && KPT >= 2 && C::HS == 0, "pipelined contains: Θ = 1, KPT >= 2, multiplicative draws");
-    const uint32_t lane = threadIdx.x & 31u;
-    SaltSrc<C> ss;
-    ss.init(0, nullptr, nullptr);
-    constexpr uint64_t TILE = 32 * KPT;
-    const uint64_t ntiles = (p.n + TILE - 1) / TILE;
-    const uint64_t nfull = p.n / TILE;
-    const uint64_t nwords = (p.n + 31) / 32;
-    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const bool vec_ok = (((uintptr_t)p.keys) & (8 * KPT - 1)) == 0;
-    const W* F = (const W*)p.words;
-    auto test = [&](const W* wd, uint32_t lo, int slot) -> uint32_t {
-        const Draws<C> dr(lo);
-        if constexpr (C::BBF_SM) return (uint32_t)test_block_sm<C>(wd, dr, ss, sm + slot * (C::B / 32) * 32);
-        else return (uint32_t)test_block<C>(wd, dr, ss);
-    };
-    if (gw < nfull) {
-        uint64_t kc[KPT];
-        load_tile_keys<KPT>(p.keys, gw * TILE + lane * KPT, vec_ok, kc);
-        uint32_t loA[H], loB[H];
-        W wa[H][C::s], wb[H][C::s];
-#pragma unroll
-        for (int j = 0; j < H; ++j) {
-            const uint64_t h = xxh64_u64(kc[j], p.seed);
-            loA[j] = (uint32_t)h;
-            load_block<C>(F, block_of(h, p.b32), wa[j]);
-        }
-        for (uint64_t t = gw; t < nfull; t += nw) {
-            const uint64_t tn = t + nw;
-            const bool have_next = tn < nfull;
-#pragma unroll
-            for (int j = 0; j < H; ++j) {
-                const uint64_t h = xxh64_u64(kc[H + j], p.seed);
-                loB[j] = (uint32_t)h;
-                load_block<C>(F, block_of(h, p.b32), wb[j]);
-            }
-            uint64_t kn[KPT];
-            if (have_next) load_tile_keys<KPT>(p.keys, tn * TILE + lane * KPT, vec_ok, kn);
-            if constexpr (C::L2PF > 0) {
-                const uint64_t tp = t + (uint64_t)C::L2PF * nw;
-                if (tp < nfull && (lane & 3u) == 0)
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.keys + tp * TILE + lane * KPT));
-            }
-            uint32_t res = 0;
-#pragma unroll
-            for (int j = 0; j < H; ++j) res |= test(wa[j], loA[j], j) << j;
-            if (have_next) {
-#pragma unroll
-                for (int j = 0; j < H; ++j) {
-                    const uint64_t h = xxh64_u64(kn[j], p.seed);
-                    loA[j] = (uint32_t)h;
-                    load_block<C>(F, block_of(h, p.b32), wa[j]);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < H; ++j) res |= test(wb[j], loB[j], H + j) << (H + j);
-            store_results<KPT>(p.out, t, res, lane, nwords);
-#pragma unroll
-            for (int j = 0; j < KPT; ++j) kc[j] = kn[j];
-        }
-    }
-    // ragged tail: at most one partial tile, taken by the warp the grid
-    // stride would give it
-    if (ntiles > nfull && gw == nfull % nw) {
-        uint64_t kin[KPT] = {}, knext[KPT];
-        run_tile<C, false, false>(p, nfull, lane, 0, 0, vec_ok, ss, kin, knext, false, 0, sm);
-    }
-}
-
 template <class C, bool ADD>
 __global__ void __launch_bounds__(256) bulk_kernel(const Params p)
 {
@@ -798,10 +706,6 @@ __global__ void __launch_bounds__(256) bulk_kernel(const Params p)
         if (threadIdx.x < 64) s_salt[threadIdx.x] = c_salt[threadIdx.x];
         if (threadIdx.x < 16) s_gsalt[threadIdx.x] = c_gsalt[threadIdx.x];
         __syncthreads();
-    }
-    if constexpr (!ADD && BF_T1_PIPE && C::THETA == 1 && C::KPT >= 2 && C::HS == 0 && C::HV == 0) {
-        contains_pipe<C>(p, sm);
-        return;
     }
     if constexpr (!ADD && C::KEY_SMEM) {
         __shared__ __align__(16) uint64_t s_keys[8 * 2 * 32 * C::KPT];
@@ -833,11 +737,6 @@ __global__ void __launch_bounds__(256) bulk_kernel(const Params p)
             const uint64_t tp = t + (uint64_t)C::L2PF * nw;
             if (tp < nfull && (lane & 3u) == 0)
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(p.keys + tp * TILE + lane * C::KPT));
-        }
-        if constexpr (BF_L1PF_DIST > 0 && !ADD) {
-            const uint64_t tp = t + (uint64_t)BF_L1PF_DIST * nw;
-            if (tp < nfull && (lane & 3u) == 0)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(p.keys + tp * TILE + lane * C::KPT));
         }
         if (t < nfull)
             run_tile<C, ADD, true>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
