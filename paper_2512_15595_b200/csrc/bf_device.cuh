@@ -171,6 +171,15 @@ __device__ __forceinline__ unsigned long long shl_clamp(unsigned long long v, ui
     return r;
 }
 
+// low 32 bits of v >> sh with PTX clamp semantics (sh >= 64, incl. wrapped
+// "negative" values, yields 0)
+__device__ __forceinline__ uint32_t shr_clamp_lo(unsigned long long v, uint32_t sh)
+{
+    unsigned long long r;
+    asm("shr.b64 %0, %1, %2;" : "=l"(r) : "l"(v), "r"(sh));
+    return (uint32_t)r;
+}
+
 // ---------------------------------------------------------------- loads
 // Streaming key loads: read once, keep out of L1 (the 256-bit form also
 // marks them evict-first in L2; ptxas accepts .L2::evict_first only there).

@@ -47,6 +47,9 @@
 #ifndef BF_L2PF_DIST
 #define BF_L2PF_DIST -1  // contains: prefetch keys this many tiles ahead into L2 (0 off, -1 rule)
 #endif
+#ifndef BF_BBF2_CLAMP
+#define BF_BBF2_CLAMP 1  // BBF over 64-bit words tests bits with clamping shifts (Cfg::BBF_CLAMP); 0 disables
+#endif
 #ifndef BF_KEY_SMEM
 #define BF_KEY_SMEM 1  // Θ=1 contains stages the key stream in shared memory (cp.async); 0 disables
 #endif
@@ -89,7 +92,14 @@ struct Cfg {
     // registers (a SEL chain of s-1 steps per draw): per-CTA staging of
     // 8 warps x KPT keys x B/32 words x 32 lanes, <= 32 KB
     static constexpr int BBF_SM_WORDS = 8 * KPT * (B / 32) * 32;
-    static constexpr bool BBF_SM = (V == V_BBF) && (B >= 256) && (BBF_SM_WORDS <= 8192);
+    // BBF contains over 2 or 4 64-bit words tests a bit as OR_i (w_i >> (p -
+    // 64 i)) with clamping shifts: no word select, no shared-memory copy.
+    // tools/kexp: BBF 128/64 +3% (k=4) to +32% (k=16); BBF 256/64 +17% (k=4),
+    // +1% (k=8), -12% (k=12: four shifts per draw lose to one LDS), hence
+    // s = 4 only up to k = 8
+    static constexpr bool BBF_CLAMP = (V == V_BBF) && (S == 64) && BF_BBF2_CLAMP &&
+                                      (s == 2 || (s == 4 && K <= 8));
+    static constexpr bool BBF_SM = (V == V_BBF) && (B >= 256) && (BBF_SM_WORDS <= 8192) && !BBF_CLAMP;
     // Θ=1 contains without the register key prefetch (PREFETCH_T1) touches the key tile two
     // grid strides ahead with prefetch.global.L2 (one request per 128-byte
     // line, no registers): the key load at the top of a tile then waits for
@@ -337,6 +347,16 @@ __device__ __forceinline__ bool test_block(const typename C::W* wd, const Draws<
                 const uint32_t d = dr.template word_draw<w0, decltype(T)::value>((uint32_t)w0, ss);
                 acc &= (uint32_t)(x >> (d >> (32 - C::LGW)));
             });
+        });
+    } else if constexpr (C::BBF_CLAMP) {
+        // s 64-bit words: bit p of the block = OR_i (w_i >> (p - 64 i)) with
+        // PTX's clamping shifts (an amount >= 64, incl. a wrapped p - 64 i,
+        // gives 0): no word select, no predicate
+        StaticFor<0, C::K>::run([&](auto J) {
+            const uint32_t p = dr.template bbf_draw<decltype(J)::value>(ss) >> (32 - C::LGB);
+            uint32_t t = shr_clamp_lo(wd[0], p);
+            StaticFor<1, C::s>::run([&](auto I) { t |= shr_clamp_lo(wd[decltype(I)::value], p - 64u * decltype(I)::value); });
+            acc &= t;
         });
     } else {  // BBF
         StaticFor<0, C::K>::run([&](auto J) {

@@ -335,6 +335,21 @@ int main(int argc, char** argv)
     CK(cudaDeviceSynchronize());
     CK(cudaEventCreate(&c.e0));
     CK(cudaEventCreate(&c.e1));
+    if (argc > 1 && strcmp(argv[1], "bbf128") == 0) {
+        run<Cfg<V_BBF, 64, 1, 4, 0, 2, 1, 4, 0>, Cfg<V_BBF, 64, 1, 4, 0, 1, 2, 4, 0>>(c, "BBF128/64 k4");
+        run<Cfg<V_BBF, 64, 1, 6, 0, 2, 1, 4, 0>, Cfg<V_BBF, 64, 1, 6, 0, 1, 2, 4, 0>>(c, "BBF128/64 k6");
+        run<Cfg<V_BBF, 64, 1, 8, 0, 2, 1, 4, 0>, Cfg<V_BBF, 64, 1, 8, 0, 1, 2, 4, 0>>(c, "BBF128/64 k8");
+        run<Cfg<V_BBF, 64, 1, 12, 0, 2, 1, 4, 0>, Cfg<V_BBF, 64, 1, 12, 0, 1, 2, 4, 0>>(c, "BBF128/64 k12");
+        run<Cfg<V_BBF, 64, 1, 16, 0, 2, 1, 4, 0>, Cfg<V_BBF, 64, 1, 16, 0, 1, 2, 4, 0>>(c, "BBF128/64 k16");
+        run<Cfg<V_BBF, 64, 2, 4, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 4, 0, 1, 4, 4, 0>>(c, "BBF256/64 k4");
+        run<Cfg<V_BBF, 64, 2, 5, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 5, 0, 1, 4, 4, 0>>(c, "BBF256/64 k5");
+        run<Cfg<V_BBF, 64, 2, 6, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 6, 0, 1, 4, 4, 0>>(c, "BBF256/64 k6");
+        run<Cfg<V_BBF, 64, 2, 7, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 7, 0, 1, 4, 4, 0>>(c, "BBF256/64 k7");
+        run<Cfg<V_BBF, 64, 2, 8, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 8, 0, 1, 4, 4, 0>>(c, "BBF256/64 k8");
+        run<Cfg<V_BBF, 64, 2, 12, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 12, 0, 1, 4, 4, 0>>(c, "BBF256/64 k12");
+        run<Cfg<V_BBF, 64, 2, 16, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 16, 0, 1, 4, 4, 0>>(c, "BBF256/64 k16");
+        return 0;
+    }
     if (argc > 1 && strcmp(argv[1], "bbfadd") == 0) {
         run<Cfg<V_BBF, 64, 2, 8, 0, 4, 1, 2, 0>, Cfg<V_BBF, 64, 2, 8, 0, 1, 4, 4, 0>>(c, "BBF256/64 k8");
         run<Cfg<V_BBF, 64, 2, 12, 0, 4, 1, 2, 0>, Cfg<V_BBF, 64, 2, 12, 0, 1, 4, 4, 0>>(c, "BBF256/64 k12");
@@ -365,6 +380,13 @@ int main(int argc, char** argv)
         run<Cfg<V_CSBF, 64, 2, 16, 2, 2, 2, 4, 0>, Cfg<V_CSBF, 64, 2, 16, 2, 1, 4, 4, 0>>(c, "CSBF256/64 z2 k16");
         run<Cfg<V_BBF, 64, 1, 8, 0, 2, 1, 4, 0>, Cfg<V_BBF, 64, 1, 8, 0, 1, 2, 4, 0>>(c, "BBF128/64 k8");
         run<Cfg<V_BBF, 64, 1, 16, 0, 2, 1, 4, 0>, Cfg<V_BBF, 64, 1, 16, 0, 1, 2, 4, 0>>(c, "BBF128/64 k16");
+        run<Cfg<V_BBF, 64, 2, 4, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 4, 0, 1, 4, 4, 0>>(c, "BBF256/64 k4");
+        run<Cfg<V_BBF, 64, 2, 5, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 5, 0, 1, 4, 4, 0>>(c, "BBF256/64 k5");
+        run<Cfg<V_BBF, 64, 2, 6, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 6, 0, 1, 4, 4, 0>>(c, "BBF256/64 k6");
+        run<Cfg<V_BBF, 64, 2, 7, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 7, 0, 1, 4, 4, 0>>(c, "BBF256/64 k7");
+        run<Cfg<V_BBF, 64, 2, 8, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 8, 0, 1, 4, 4, 0>>(c, "BBF256/64 k8");
+        run<Cfg<V_BBF, 64, 2, 12, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 12, 0, 1, 4, 4, 0>>(c, "BBF256/64 k12");
+        run<Cfg<V_BBF, 64, 2, 16, 0, 4, 1, 4, 0>, Cfg<V_BBF, 64, 2, 16, 0, 1, 4, 4, 0>>(c, "BBF256/64 k16");
         return 0;
     }
     if (argc > 1 && strcmp(argv[1], "ts") == 0) {
