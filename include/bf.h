@@ -111,7 +111,7 @@ int bf_contains(const bf_filter* f, const uint64_t* keys, uint64_t n,
  * The library streams them through internal device staging buffers in
  * chunks, overlapping the host->device copies with the kernels on `stream`.
  * These calls synchronize `stream` before returning (the host result is
- * ready on return). */
+ * ready on return).  A partitioned filter (nparts > 1) returns BF_EINVAL. */
 int bf_add_host(bf_filter* f, const uint64_t* host_keys, uint64_t n, void* stream);
 int bf_contains_host(const bf_filter* f, const uint64_t* host_keys, uint64_t n,
                      uint32_t* host_out_bits, void* stream);
@@ -206,7 +206,8 @@ int bf_part_info(const bf_filter* f, uint32_t* nparts, uint32_t* part, uint64_t*
 int bf_route(const bf_filter* f, const uint64_t* keys, uint64_t n, uint64_t idx_base,
              uint64_t* recs, uint64_t* idx, uint64_t cap, unsigned long long* counts, void* stream);
 /* OR the routed records of nsrc source buckets (recs[s*cap ..], counts[s])
- * into this part. */
+ * into this part.  recs must be 32-byte aligned (256-bit record loads;
+ * BF_EINVAL otherwise). */
 int bf_add_routed(bf_filter* f, const uint64_t* recs, const unsigned long long* counts,
                   uint32_t nsrc, uint64_t cap, void* stream);
 /* Test routed records against this part: res[s*cap + j] = 1 / 0. */
@@ -239,7 +240,8 @@ int bf_keygen(uint64_t* out, uint64_t n, uint64_t base_index, void* stream);
  *   probe_red:  `lanes` lanes (1 .. block_bits/64) each issue one 64-bit
  *               red.global.or of a key-derived bit into their word of the
  *               block (like bf_add with Θ = lanes).
- * buf: device pointer to b*block_bits/8 bytes. */
+ * buf: device pointer to b*block_bits/8 bytes.  probe_read needs keys 32-byte
+ * aligned (256-bit key loads) and out_bits 4-byte aligned (BF_EINVAL). */
 int bf_probe_read(const void* buf, uint64_t b, uint32_t block_bits, const uint64_t* keys,
                   uint64_t n, uint32_t* out_bits, void* stream);
 int bf_probe_red(void* buf, uint64_t b, uint32_t block_bits, uint32_t lanes,

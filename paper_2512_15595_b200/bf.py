@@ -123,6 +123,43 @@ def _ptr(x) -> int:
     return int(x.data_ptr()) if hasattr(x, "data_ptr") else int(x)
 
 
+def _check_keys(keys, n: int, on_device: bool, device=None) -> None:
+    """Tensor arguments must be what the C ABI reads: n contiguous 64-bit
+    keys on the right side of PCIe (raw pointers pass through unchecked)."""
+    if not hasattr(keys, "data_ptr"):
+        return
+    import torch
+    if keys.dtype not in (torch.int64, getattr(torch, "uint64", torch.int64)):
+        raise ValueError(f"keys must be int64/uint64 (got {keys.dtype}): the kernels read 8 bytes per key")
+    if not keys.is_contiguous():
+        raise ValueError("keys must be contiguous")
+    if n > keys.numel():
+        raise ValueError(f"n = {n} exceeds the {keys.numel()} keys given")
+    if on_device and not keys.is_cuda:
+        raise ValueError("keys must be a CUDA tensor (use add_host / contains_host for host buffers)")
+    if not on_device and keys.is_cuda:
+        raise ValueError("host-buffer call: keys must be a CPU (preferably pinned) tensor")
+    if on_device and device is not None and keys.device.index != device:
+        raise ValueError(f"keys are on cuda:{keys.device.index}, the filter on cuda:{device}")
+
+
+def _check_out(out, n: int, on_device: bool, device=None) -> None:
+    if not hasattr(out, "data_ptr"):
+        return
+    import torch
+    if out.dtype not in (torch.int32, getattr(torch, "uint32", torch.int32)):
+        raise ValueError(f"out_bits must be int32/uint32 (got {out.dtype})")
+    if not out.is_contiguous():
+        raise ValueError("out_bits must be contiguous")
+    if out.numel() < (n + 31) // 32:
+        raise ValueError(f"out_bits holds {out.numel()} words, {(n + 31) // 32} needed for {n} keys")
+    if on_device != out.is_cuda:
+        raise ValueError("out_bits must live where the call writes it (CUDA tensor for bf_contains, "
+                         "host tensor for bf_contains_host)")
+    if on_device and device is not None and out.device.index != device:
+        raise ValueError(f"out_bits is on cuda:{out.device.index}, the filter on cuda:{device}")
+
+
 # ---------------------------------------------------------------- C names
 def bf_create(m_bits: int, k: int, block_bits: int, word_bits: int, variant: int, seed: int = 0) -> int:
     h = _lib.bf_create_seeded(m_bits, k, block_bits, word_bits, variant, seed)
@@ -134,21 +171,27 @@ def bf_create(m_bits: int, k: int, block_bits: int, word_bits: int, variant: int
 
 def bf_add(f: int, keys, n: int | None = None, stream=None) -> None:
     n = keys.numel() if n is None else n
+    _check_keys(keys, n, True)
     _check(_lib.bf_add(f, _ptr(keys), n, _stream(stream)))
 
 
 def bf_contains(f: int, keys, out_bits, n: int | None = None, stream=None) -> None:
     n = keys.numel() if n is None else n
+    _check_keys(keys, n, True)
+    _check_out(out_bits, n, True)
     _check(_lib.bf_contains(f, _ptr(keys), n, _ptr(out_bits), _stream(stream)))
 
 
 def bf_add_host(f: int, host_keys, n: int | None = None, stream=None) -> None:
     n = host_keys.numel() if n is None else n
+    _check_keys(host_keys, n, False)
     _check(_lib.bf_add_host(f, _ptr(host_keys), n, _stream(stream)))
 
 
 def bf_contains_host(f: int, host_keys, host_out_bits, n: int | None = None, stream=None) -> None:
     n = host_keys.numel() if n is None else n
+    _check_keys(host_keys, n, False)
+    _check_out(host_out_bits, n, False)
     _check(_lib.bf_contains_host(f, _ptr(host_keys), n, _ptr(host_out_bits), _stream(stream)))
 
 
@@ -340,6 +383,8 @@ class Filter:
         v |= BF_SCHEME(scheme)
         self.m_bits, self.k, self.B, self.S = m_bits, k, block_bits, word_bits
         self.variant, self.z, self.seed = v & 0xFF, z, seed
+        import torch
+        self.device = torch.cuda.current_device() if torch.cuda.is_available() else None
         self.handle = bf_create(m_bits, k, block_bits, word_bits, v, seed)
         self.b, self.s, self.m_eff = bf_geometry(self.handle)
 
@@ -353,6 +398,7 @@ class Filter:
             self.handle = None
 
     def add(self, keys, stream=None):
+        _check_keys(keys, keys.numel(), True, self.device)
         bf_add(self.handle, keys, keys.numel(), stream)
 
     def contains(self, keys, out=None, stream=None):
@@ -360,6 +406,8 @@ class Filter:
         n = keys.numel()
         if out is None:
             out = torch.empty((n + 31) // 32, dtype=torch.int32, device=keys.device)
+        _check_keys(keys, n, True, self.device)
+        _check_out(out, n, True, self.device)
         bf_contains(self.handle, keys, out, n, stream)
         return out
 

@@ -5,6 +5,13 @@ parallel (one nvcc per translation unit) and links them into
 paper_2512_15595_b200/libbf200.so (in-tree, so it travels with the repo to the
 GPU box).  Incremental: a translation unit is rebuilt only if a source or
 header is newer than its object.
+
+-lineinfo: the hand-written translation units always carry it.  The generated
+specializations (~1,200 kernels) carry it only in the profiling build
+(`python -m paper_2512_15595_b200.build --lineinfo` ->
+libbf200_lineinfo.so, selected with BF200_LIB=... for ncu --import-source
+captures): with -lineinfo ptxas embeds the PTX text of every kernel twice,
+which made the default library 4x larger (126 MB) for no run-time effect.
 """
 from __future__ import annotations
 
@@ -21,7 +28,8 @@ LIB = os.path.join(PKG, "libbf200.so")
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-I", INCLUDE, "-I", CSRC]
+LIB_LINEINFO = os.path.join(PKG, "libbf200_lineinfo.so")
+FLAGS = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", INCLUDE, "-I", CSRC]
 
 
 def _headers():
@@ -38,11 +46,15 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu"))) + shards
 
 
-def _compile(src, hdr_mtime, verbose):
-    obj = os.path.join(OBJ, os.path.relpath(src, CSRC).replace(os.sep, "_") + ".o")
+def _compile(src, hdr_mtime, verbose, lineinfo_all=False):
+    gen = os.sep + "gen" + os.sep in src
+    lineinfo = lineinfo_all or not gen
+    sub = OBJ + ("_li" if lineinfo_all and gen else "")
+    os.makedirs(sub, exist_ok=True)
+    obj = os.path.join(sub, os.path.relpath(src, CSRC).replace(os.sep, "_") + ".o")
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime):
         return obj, False
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj + ".tmp"]
+    cmd = [NVCC, *ARCH, *FLAGS, *(["-lineinfo"] if lineinfo else []), "-c", src, "-o", obj + ".tmp"]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -52,24 +64,25 @@ def _compile(src, hdr_mtime, verbose):
     return obj, True
 
 
-def build(verbose: bool = False, jobs: int | None = None) -> str:
+def build(verbose: bool = False, jobs: int | None = None, lineinfo: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     srcs = sources()
     hdr = max(os.path.getmtime(h) for h in _headers())
     jobs = jobs or max(1, min(len(srcs), os.cpu_count() or 4))
     with ThreadPoolExecutor(jobs) as ex:
-        res = list(ex.map(lambda s: _compile(s, hdr, verbose), srcs))
+        res = list(ex.map(lambda s: _compile(s, hdr, verbose, lineinfo), srcs))
     objs = [o for o, _ in res]
-    if any(c for _, c in res) or not os.path.exists(LIB) or \
-            any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        tmp = LIB + f".tmp{os.getpid()}"
+    lib = LIB_LINEINFO if lineinfo else LIB
+    if any(c for _, c in res) or not os.path.exists(lib) or \
+            any(os.path.getmtime(o) > os.path.getmtime(lib) for o in objs):
+        tmp = lib + f".tmp{os.getpid()}"
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, lineinfo="--lineinfo" in sys.argv))

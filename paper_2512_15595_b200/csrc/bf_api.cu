@@ -456,6 +456,9 @@ static Params make_params(const bf_filter* f, const uint64_t* keys, uint64_t n, 
 
 static int launch_bulk(const bf_filter* f, int op, const uint64_t* keys, uint64_t n, uint32_t* out, cudaStream_t st)
 {
+    // a part holds only blocks [blk_lo, blk_hi) of a b_global-block filter:
+    // the bulk kernels index blocks globally, so they must never see one
+    if (f->nparts > 1) return fail(BF_EINVAL, "partitioned filter: route keys with bf_route first");
     const Sched& sc = f->sched[op];
     const uint64_t tile_keys = sc.specialized ? 32ULL * sc.kpt : 32ULL;
     const uint64_t tiles = (n + tile_keys - 1) / tile_keys;
@@ -753,6 +756,7 @@ int bf_add_routed(bf_filter* f, const uint64_t* recs, const unsigned long long* 
                   void* stream)
 {
     if (!f || !recs || !counts || nsrc < 1 || cap == 0 || (cap & 127)) return fail(BF_EINVAL, "bf_add_routed: bad arguments");
+    if ((uintptr_t)recs & 31) return fail(BF_EINVAL, "bf_add_routed: recs must be 32-byte aligned (256-bit record loads)");
     KernelFn bin_fn, apply_fn, test_fn;
     if (!routed_kernels(f, &bin_fn, &apply_fn, &test_fn))
         return fail(BF_EUNSUPPORTED, "routing kernels are not compiled for this configuration");
@@ -868,6 +872,7 @@ int bf_add_host(bf_filter* f, const uint64_t* host_keys, uint64_t n, void* strea
 {
     if (!f) return fail(BF_EINVAL, "null filter");
     if (n == 0) return BF_OK;
+    if (f->nparts > 1) return fail(BF_EINVAL, "partitioned filter: route keys with bf_route, then bf_add_routed");
     if (!host_keys) return fail(BF_EINVAL, "null host keys");
     DeviceGuard g(f->device);
     return host_bulk(f, 0, host_keys, n, nullptr, (cudaStream_t)stream);
@@ -877,6 +882,7 @@ int bf_contains_host(const bf_filter* f, const uint64_t* host_keys, uint64_t n, 
 {
     if (!f) return fail(BF_EINVAL, "null filter");
     if (n == 0) return BF_OK;
+    if (f->nparts > 1) return fail(BF_EINVAL, "partitioned filter: route keys with bf_route, then bf_contains_routed");
     if (!host_keys || !host_out_bits) return fail(BF_EINVAL, "null host buffer");
     DeviceGuard g(f->device);
     return host_bulk((bf_filter*)f, 1, host_keys, n, host_out_bits, (cudaStream_t)stream);
@@ -908,8 +914,8 @@ int bf_probe_read(const void* buf, uint64_t b, uint32_t block_bits, const uint64
                   uint32_t* out_bits, void* stream)
 {
     if (n == 0) return BF_OK;
-    if (!buf || !keys || !out_bits || b < 1 || b > (1ULL << 32) || ((uintptr_t)keys & 7))
-        return fail(BF_EINVAL, "bf_probe_read: bad arguments");
+    if (!buf || !keys || !out_bits || b < 1 || b > (1ULL << 32) || ((uintptr_t)keys & 31) || ((uintptr_t)out_bits & 3))
+        return fail(BF_EINVAL, "bf_probe_read: bad arguments (keys must be 32-byte aligned: 256-bit key loads)");
     int dev = 0;
     cudaGetDevice(&dev);
     if (launch_probe_read(buf, b, block_bits, keys, n, out_bits, (cudaStream_t)stream, 8 * sm_count(dev)))

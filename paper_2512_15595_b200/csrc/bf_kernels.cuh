@@ -40,19 +40,7 @@
 
 #include "bf_device.cuh"
 
-// Experiment knobs (tools/kexp): compile-time overrides of schedule rules.
-#ifndef BF_T1_PF_MODE
-#define BF_T1_PF_MODE 0  // Θ=1 contains key prefetch into registers: 0 rule, 1 always, 2 never
-#endif
-#ifndef BF_L2PF_DIST
-#define BF_L2PF_DIST -1  // contains: prefetch keys this many tiles ahead into L2 (0 off, -1 rule)
-#endif
-#ifndef BF_BBF2_CLAMP
-#define BF_BBF2_CLAMP 1  // BBF over 64-bit words tests bits with clamping shifts (Cfg::BBF_CLAMP); 0 disables
-#endif
-#ifndef BF_KEY_SMEM
-#define BF_KEY_SMEM 1  // Θ=1 contains stages the key stream in shared memory (cp.async); 0 disables
-#endif
+#include <bf_tuning.h>  // angle brackets: tools/kexp substitutes its own copy via -I
 
 namespace bf {
 
@@ -86,7 +74,7 @@ struct Cfg {
     // flight only when the KPT loaded blocks leave room for them
     // (KPT*s*S/32 registers); add and cooperative contains always do
     static constexpr bool PREFETCH_T1 =
-        BF_T1_PF_MODE == 1 ? true : (BF_T1_PF_MODE == 2 ? false : (KPT * s * S / 32 <= 16));
+        tuning::T1_PF_MODE == 1 ? true : (tuning::T1_PF_MODE == 2 ? false : (KPT * s * S / 32 <= 16));
     // BBF contains (Θ = 1) with B >= 256 tests its draws against a copy of
     // the block in shared memory instead of selecting the word among s
     // registers (a SEL chain of s-1 steps per draw): per-CTA staging of
@@ -97,7 +85,7 @@ struct Cfg {
     // tools/kexp: BBF 128/64 +3% (k=4) to +32% (k=16); BBF 256/64 +17% (k=4),
     // +1% (k=8), -12% (k=12: four shifts per draw lose to one LDS), hence
     // s = 4 only up to k = 8
-    static constexpr bool BBF_CLAMP = (V == V_BBF) && (S == 64) && BF_BBF2_CLAMP &&
+    static constexpr bool BBF_CLAMP = (V == V_BBF) && (S == 64) && tuning::BBF2_CLAMP &&
                                       (s == 2 || (s == 4 && K <= 8));
     static constexpr bool BBF_SM = (V == V_BBF) && (B >= 256) && (BBF_SM_WORDS <= 8192) && !BBF_CLAMP;
     // Θ=1 contains without the register key prefetch (PREFETCH_T1) touches the key tile two
@@ -114,9 +102,9 @@ struct Cfg {
     // in shared memory gain from it only at k >= 12 (BBF 256/64 k=8 -7%,
     // k=16 +7%: the two staging areas cost a CTA per SM)
     static constexpr bool KEY_SMEM =
-        BF_KEY_SMEM && THETA == 1 && KPT % 2 == 0 && !PREFETCH_T1 && (!BBF_SM || K >= 12);
+        tuning::KEY_SMEM && THETA == 1 && KPT % 2 == 0 && !PREFETCH_T1 && (!BBF_SM || K >= 12);
     static constexpr int L2PF =
-        BF_L2PF_DIST >= 0 ? BF_L2PF_DIST : ((THETA == 1 && !PREFETCH_T1 && !BBF_SM && B <= 256) ? 2 : 0);
+        tuning::L2PF_DIST >= 0 ? tuning::L2PF_DIST : ((THETA == 1 && !PREFETCH_T1 && !BBF_SM && B <= 256) ? 2 : 0);
     // BBF add (Θ > 1) with B >= 256: each lane ORs its own keys' whole
     // patterns into shared memory (one atomic per draw) and the group then
     // issues the coalesced REDs from there, instead of every lane of the group

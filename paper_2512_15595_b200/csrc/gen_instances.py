@@ -45,16 +45,36 @@ def default_add(v, B, S, z):
     return s, 1
 
 
+def _layout_module():
+    """paper_2512_15595_b200/layout.py (the Θ/Φ layout algebra),
+    loaded by path: this script runs standalone from csrc/."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bf_layout", os.path.join(os.path.dirname(HERE), "layout.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
 def layouts(s):
-    out = []
-    t = 1
-    while t <= s:
-        p = 1
-        while t * p <= s:
-            out.append((t, p))
-            p *= 2
-        t *= 2
-    return out
+    return _layout_module().enumerate_layouts(s)
+
+
+# configs[1] sweep geometries (SURVEY 8(d) C2): (variant, B, S, z), k = 4..16 where valid
+C2_GEOMS = [(RBBF, 32, 32, 0), (RBBF, 64, 64, 0), (SBF, 64, 32, 0), (SBF, 128, 64, 0),
+            (SBF, 128, 32, 0), (SBF, 256, 64, 0), (SBF, 256, 32, 0), (BBF, 128, 64, 0),
+            (BBF, 256, 64, 0), (CSBF, 256, 32, 2), (CSBF, 256, 32, 4), (CSBF, 256, 64, 2)]
+
+
+# rows reported with the sweep besides the 94 above: BBF with 32-bit words and
+# a one-word BBF (the equivalence checks' geometries), BBF 256/32 at configs[3]'s
+# other iso-FPR point (SURVEY App. C)
+C2_EXTRA = [(BBF, 64, 64, 8, 0), (BBF, 256, 32, 8, 0), (BBF, 256, 32, 11, 0)]
+
+
+def c2_rows(extra: bool = True):
+    """The (variant, B, S, k, z) rows of the configs[1] sweep: 94 + 3 extra = 97."""
+    rows = [(v, B, S, k, z) for v, B, S, z in C2_GEOMS for k in valid_k(v, B, S, z, range(4, 17))]
+    return rows + (C2_EXTRA if extra else [])
 
 
 def instances():
@@ -63,10 +83,13 @@ def instances():
     def add(op, v, B, S, k, z, theta, phi, kpt, hv):
         inst.add((op, v, B, S, k, z, theta, phi, kpt, hv))
 
-    def defaults(v, B, S, k, z, kpts=(1, 2, 4)):
+    def defaults(v, B, S, k, z, kpts=(2, 4)):
+        """Default layouts plus the few alternatives the configs[1] sweep
+        ever picked (profiles/r1_results_c2.md): contains wins at KPT = 4 on
+        all 97 rows, add at KPT = 2 or 4 (KPT = 1 never by more than 4%)."""
         s = B // S
+        add(1, v, B, S, k, z, 1, s, 4, 0)   # contains: Θ=1, Φ=s (P:L342)
         for kpt in kpts:
-            add(1, v, B, S, k, z, 1, s, kpt, 0)   # contains: Θ=1, Φ=s
             add(0, v, B, S, k, z, s, 1, kpt, 0)   # add: Θ=s, Φ=1 (P:L344)
             if s > 1:
                 add(0, v, B, S, k, z, 1, s, kpt, 0)  # add Θ=1 (BBF/CSBF may prefer it)
@@ -74,17 +97,12 @@ def instances():
                 # one lane per group (Θ = z, Φ = s/z): group-wise masks (Cfg::GROUPWISE)
                 add(0, v, B, S, k, z, z, s // z, kpt, 0)
                 add(1, v, B, S, k, z, z, s // z, kpt, 0)
+        if s >= 4:  # add Θ = s/2, Φ = 2 (picked for some BBF/CSBF rows)
+            add(0, v, B, S, k, z, s // 2, 2, 4, 0)
 
     # configs[1] sweep rows, k = 4..16 where valid
-    rows = [(RBBF, 32, 32, 0), (RBBF, 64, 64, 0), (SBF, 64, 32, 0), (SBF, 128, 64, 0),
-            (SBF, 128, 32, 0), (SBF, 256, 64, 0), (SBF, 256, 32, 0), (BBF, 128, 64, 0),
-            (BBF, 256, 64, 0), (CSBF, 256, 32, 2), (CSBF, 256, 32, 4), (CSBF, 256, 64, 2)]
-    for v, B, S, z in rows:
-        for k in valid_k(v, B, S, z, range(4, 17)):
-            defaults(v, B, S, k, z)
-    # BBF with 32-bit words (same bytes as S=64) for the equivalence tests
-    defaults(BBF, 256, 32, 8, 0, kpts=(4,))
-    defaults(BBF, 64, 64, 8, 0, kpts=(4,))
+    for v, B, S, k, z in c2_rows():
+        defaults(v, B, S, k, z)
     # configs[3]: SBF 256/32 at k = 16 and 8: every layout x KPT, hash variants
     for k in (8, 16):
         for op in (0, 1):
@@ -94,7 +112,7 @@ def instances():
                 for hv in (1, 2, 3):
                     add(op, SBF, 256, 32, k, 0, theta, phi, 1, hv)
     # companions of configs[3] at its other iso-FPR points
-    for v, B, S, k, z in [(SBF, 256, 64, 12, 0), (BBF, 256, 32, 11, 0), (CSBF, 256, 32, 12, 4)]:
+    for v, B, S, k, z in [(SBF, 256, 64, 12, 0), (CSBF, 256, 32, 12, 4)]:
         defaults(v, B, S, k, z)
     # the paper's Table 1/2 grid: SBF, S=64, k=16, B=64..1024, every Θ
     # with the maximal Φ = s/Θ, KPT 1/2/4 -- includes the B=512/1024 blocks (NEXT N2)
@@ -113,7 +131,7 @@ def instances():
         for z in (2, 4, 8, 16):
             if z > s:
                 continue
-            defaults(CSBF, B, 64, 16, z, kpts=(1, 4))
+            defaults(CSBF, B, 64, 16, z, kpts=(4,))
             for t in sorted({max(1, B // 256), z}):
                 if t <= s:
                     add(1, CSBF, B, 64, 16, z, t, s // t, 1, 0)
@@ -134,6 +152,13 @@ def scheme_instances():
             if op == 0 and s > 1:
                 out.append((op, v, B, S, k, 0, s, 1, 4, 0, 1))  # double hashing, add Θ = s
     return out
+
+
+# the N4 hybrid TMA+LSU add (measured slower than the LSU add everywhere,
+# DESIGN.md section 8) is kept for these configurations only
+# (tests/test_gpu_parity.py HYBRID_CFGS, tools/sweep.py --set n4)
+HYBRID = {(SBF, 256, 64, 8, 0), (SBF, 256, 32, 16, 0), (BBF, 256, 64, 8, 0), (CSBF, 256, 32, 8, 2),
+          (SBF, 128, 64, 8, 0), (SBF, 512, 64, 16, 0), (SBF, 1024, 64, 16, 0), (CSBF, 1024, 64, 16, 4)}
 
 
 def cfg_type(i):
@@ -158,8 +183,8 @@ def emit():
             binned.append((2, v, B, S, k, z, 1, 1, 1, 0))
             binned.append((3, v, B, S, k, z, theta, phi, kpt, hv))
             binned.append((4, v, B, S, k, z, 1, B // S, 1, 0))  # routed contains (Θ=1, Φ=s)
-            if B >= 128:
-                binned.append((5, v, B, S, k, z, theta, phi, kpt, hv))  # hybrid TMA+LSU add
+            if (v, B, S, k, z) in HYBRID:
+                binned.append((5, v, B, S, k, z, theta, phi, kpt, hv))  # hybrid TMA+LSU add (N4 experiment)
     inst = inst + binned + scheme_instances()
     shards = [inst[i::NSHARDS] for i in range(NSHARDS)]
     for si, sh in enumerate(shards):

@@ -294,12 +294,13 @@ class PartitionedFilter:
     """One rank's part of a block-range partitioned filter."""
 
     def __init__(self, m_bits: int, k: int, block_bits: int = 256, word_bits: int = 64, variant: int = 3,
-                 z: int = 0, seed: int = 0, group=None, ops=None, slack: float = 0.05):
+                 z: int = 0, seed: int = 0, group=None, ops=None, slack: float = 0.05,
+                 pad: int = 4096):
         from . import bf
         self.group = group
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.slack = slack
+        self.slack, self.pad = slack, pad
         if ops is None:
             v = variant | (z << 8) if variant == bf.BF_CSBF else variant
             self.handle = bf.bf_create_part(m_bits, k, block_bits, word_bits, v, seed, self.P, self.rank)
@@ -320,7 +321,7 @@ class PartitionedFilter:
         t = torch.tensor([n], dtype=torch.int64, device=self._dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         nmax = int(t.item())
-        cap = int(nmax / self.P * (1 + self.slack)) + 4096
+        cap = int(nmax / self.P * (1 + self.slack)) + self.pad
         return (cap + 127) // 128 * 128
 
     def _exchange(self, send, P, cap):
@@ -328,15 +329,29 @@ class PartitionedFilter:
         dist.all_to_all_single(recv, send, group=self.group)
         return recv
 
-    def _check(self, counts, cap):
-        if int(counts.max().item()) > cap:
-            raise RuntimeError("routing bucket overflow; raise `slack`")
+    def _route_agreed(self, keys, want_idx):
+        """Route, then agree COLLECTIVELY on whether any (sender, owner)
+        bucket overflowed: every rank all-reduces (MAX) its largest count, so
+        all ranks see the same number and either all proceed to the
+        exchange or all re-route with a larger cap (a skewed or
+        duplicate-heavy shard would otherwise raise on one rank while the
+        others wait in all_to_all, or drop records: false negatives).
+        bf_route counts every record, also those past cap, so one retry
+        always suffices."""
+        P, cap = self.P, self._cap(keys.numel())
+        while True:
+            recs, idx, counts = self.ops.route(keys, cap, P, want_idx)
+            t = counts.max().reshape(1).to(torch.int64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+            need = int(t.item())
+            if need <= cap:
+                return recs, idx, counts, cap
+            cap = (int(need * (1 + self.slack)) + 127) // 128 * 128
 
     def add(self, keys: torch.Tensor) -> None:
         self._dev = keys.device
-        P, cap = self.P, self._cap(keys.numel())
-        recs, _, counts = self.ops.route(keys, cap, P, False)
-        self._check(counts, cap)
+        P = self.P
+        recs, _, counts, cap = self._route_agreed(keys, False)
         recv = self._exchange(recs, P, cap)
         rcounts = self._exchange(counts, P, 1)
         self.ops.add_routed(recv, rcounts, P, cap)
@@ -365,9 +380,8 @@ class PartitionedFilter:
 
     def contains(self, keys: torch.Tensor) -> torch.Tensor:
         self._dev = keys.device
-        P, cap = self.P, self._cap(keys.numel())
-        recs, idx, counts = self.ops.route(keys, cap, P, True)
-        self._check(counts, cap)
+        P = self.P
+        recs, idx, counts, cap = self._route_agreed(keys, True)
         recv = self._exchange(recs, P, cap)
         rcounts = self._exchange(counts, P, 1)
         res = self.ops.contains_routed(recv, rcounts, P, cap)

@@ -15,21 +15,13 @@ from __future__ import annotations
 
 import statistics
 
-from . import bf
+from . import bf, layout
 
 
 def candidate_layouts(s: int):
-    """Every (Θ, Φ, KPT) the ABI accepts for a block of s words."""
-    out = []
-    t = 1
-    while t <= s:
-        p = 1
-        while t * p <= s:
-            for kpt in (1, 2, 4):
-                out.append((t, p, kpt))
-            p *= 2
-        t *= 2
-    return out
+    """Every (Θ, Φ, KPT) the ABI accepts for a block of s words (the layout
+    algebra of layout.py; KPT 1/2/4)."""
+    return [(t, p, kpt) for t, p in layout.enumerate_layouts(s) for kpt in (1, 2, 4)]
 
 
 def autotune(f: "bf.Filter", op: int, n: int = 1 << 24, reps: int = 5, allow_clear: bool = False,

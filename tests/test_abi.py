@@ -68,7 +68,11 @@ def test_instantiation_table_matches_generator(bflib):
     assert len(inst) > 500
     # every configs[1] sweep row has both default layouts compiled
     assert (1, 3, 256, 64, 8, 0, 1, 4, 4, 0) in inst  # contains SBF 256/64 k8 Θ1 Φ4 kpt4
-    assert (0, 3, 256, 64, 8, 0, 4, 1, 1, 0) in inst  # add SBF 256/64 k8 Θ4 Φ1
+    assert (0, 3, 256, 64, 8, 0, 4, 1, 4, 0) in inst  # add SBF 256/64 k8 Θ4 Φ1 kpt4
+    for v, B, S, k, z in g.c2_rows():  # all 97 rows: default add (Θ=s or Θ=z) and contains, KPT = 4
+        s = B // S
+        th, ph = g.default_add(v, B, S, z)
+        assert (0, v, B, S, k, z, th, ph, 4, 0) in inst and (1, v, B, S, k, z, 1, s, 4, 0) in inst
 
 
 def _build_demo():
@@ -157,3 +161,26 @@ def test_null_handle_calls_fail_cleanly(bflib):
     L.bf_destroy.argtypes = [ctypes.c_void_p]
     L.bf_destroy(None)  # NULL-safe
     assert bflib.last_error()[0] in (bflib.BF_EINVAL, bflib.BF_OK)
+
+
+def test_binding_rejects_bad_tensors(bflib):
+    """The binding validates tensor arguments before the C ABI sees a raw
+    pointer: 32-bit keys (the kernel would read twice the
+    buffer), strided views, device/host mismatches and short outputs."""
+    import torch
+    bf = bflib
+    k64 = torch.zeros(64, dtype=torch.int64)
+    bad = [
+        lambda: bf.bf_add(0, torch.zeros(64, dtype=torch.int32)),
+        lambda: bf.bf_add(0, torch.zeros(128, dtype=torch.int64)[::2]),
+        lambda: bf.bf_add(0, k64),                          # host tensor to the device call
+        lambda: bf.bf_add(0, k64, 65),                      # n beyond the tensor
+        lambda: bf.bf_contains(0, k64, torch.zeros(2, dtype=torch.int32)),
+        lambda: bf.bf_add_host(0, torch.zeros(64, dtype=torch.float64)),
+        lambda: bf.bf_contains_host(0, k64, torch.zeros(1, dtype=torch.int32)),   # 2 words needed
+        lambda: bf.bf_contains_host(0, k64, torch.zeros(2, dtype=torch.int64)),   # wrong dtype
+    ]
+    for i, fn in enumerate(bad):
+        with pytest.raises(ValueError):
+            fn()
+            pytest.fail(f"case {i} accepted")

@@ -129,3 +129,48 @@ def test_partitioned_filter_matches_single(world):
     m_bits = 256 * 1003  # b = 1003 blocks: uneven parts
     mp.spawn(_worker, args=(world, _free_port(), m_bits, results), nprocs=world, join=True)
     assert dict(results) == {r: (True, True) for r in range(world)}
+
+
+def _skew_worker(rank, world, port, m_bits, results):
+    """Rank 0's shard lands entirely in owner 0's block range, so only rank 0
+    overflows the first cap: every rank must agree to re-route (collective
+    MAX of the counts) instead of rank 0 raising while the others wait in
+    all_to_all, and no record may be dropped."""
+    import torch.distributed as dist
+
+    import synth
+    from oracle.bfo import OracleFilter
+    from paper_2512_15595_b200.dist import PartitionedFilter
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        geom = OracleFilter(3, m_bits, B=256, S=64, k=8, allocate=False)
+        ops = OracleRouteOps(geom, world, rank)
+        pf = PartitionedFilter(m_bits, 8, 256, 64, 3, group=None, ops=ops, slack=0.05, pad=0)
+        cand = synth.keys(777, 4000)
+        hot = np.array([k for k in cand if ops.owner(geom.pattern(int(k))[0]) == 0], dtype=np.uint64)
+        mine = hot[:600] if rank == 0 else synth.keys(50_000 * rank, 600)
+        pf.add(torch.from_numpy(mine.view(np.int64)))
+        parts = [None] * world
+        dist.all_gather_object(parts, ops.bits)
+        full = OracleFilter(3, m_bits, B=256, S=64, k=8)
+        full.add(hot[:600])
+        for r in range(1, world):
+            full.add(synth.keys(50_000 * r, 600))
+        want_bits = np.unpackbits(full.bytes(), bitorder="little")
+        q = np.concatenate([mine, synth.negatives(300, offset=rank * 1000)])
+        got = pf.contains(torch.from_numpy(q.view(np.int64)))
+        want = np.unpackbits(full.contains(q).view(np.uint8), bitorder="little")[: q.size]
+        results[rank] = (bool(np.array_equal(np.concatenate(parts), want_bits)), bool(np.array_equal(got, want)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_bucket_overflow_is_agreed_collectively(world):
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_skew_worker, args=(world, _free_port(), 256 * 1003, results), nprocs=world, join=True)
+    assert dict(results) == {r: (True, True) for r in range(world)}

@@ -1,0 +1,24 @@
+// Experiment copy of paper_2512_15595_b200/csrc/bf_tuning.h for tools/kexp:
+// build.sh puts this directory first on the include path, so -DBF_... flags
+// override the product's measured schedule rules in the harness only.
+#pragma once
+#ifndef BF_T1_PF_MODE
+#define BF_T1_PF_MODE 0
+#endif
+#ifndef BF_L2PF_DIST
+#define BF_L2PF_DIST -1
+#endif
+#ifndef BF_BBF2_CLAMP
+#define BF_BBF2_CLAMP 1
+#endif
+#ifndef BF_KEY_SMEM
+#define BF_KEY_SMEM 1
+#endif
+namespace bf {
+namespace tuning {
+constexpr int T1_PF_MODE = BF_T1_PF_MODE;
+constexpr int L2PF_DIST = BF_L2PF_DIST;
+constexpr bool BBF2_CLAMP = BF_BBF2_CLAMP;
+constexpr bool KEY_SMEM = BF_KEY_SMEM;
+}  // namespace tuning
+}  // namespace bf
