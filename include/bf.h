@@ -260,6 +260,26 @@ int bf_probe_red(void* buf, uint64_t b, uint32_t block_bits, uint32_t lanes,
 int bf_probe_rng(void* buf, uint64_t b, uint32_t block_bits, int red, uint32_t lanes, uint64_t n,
                  void* stream);
 
+/* GUPS-style random-access probes (the paper's speed of light: "random
+ * 64-bit loads / updates", P:L340 footnote): n accesses at addresses
+ * uniform over the nbytes buffer (64-byte aligned), 8 independent accesses in
+ * flight per thread, addresses from an in-register xorshift stream.
+ *   red = 0: loads of access_bytes in {8, 32, 64}; hint 0 none, 1 .L2::64B,
+ *            2 .L2::128B (not with 64-byte accesses) -- the L2 fill-size hint
+ *   red = 1: red.global.or.b64 of one random 8-byte word (access_bytes 8,
+ *            hint 0)
+ * Results are discarded; the buffer is read or OR-ed. */
+int bf_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint64_t n,
+                  void* stream);
+
+/* The current device's L2 fetch granularity for DRAM misses
+ * (cudaLimitMaxL2FetchGranularity, a context-wide hint): bytes in
+ * {32, 64, 128}, or 0 to restore the value the context started with.  The
+ * library never changes it on its own; tests and bench.py measure its effect
+ * on HBM-resident filters. */
+int bf_set_l2_fetch_granularity(uint32_t bytes);
+int bf_get_l2_fetch_granularity(uint32_t* bytes);
+
 /* ---- In-switch OR merge over NVLink SHARP ----
  *
  * Merging P partial filters built on P GPUs ("insertions ...

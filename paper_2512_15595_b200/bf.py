@@ -58,6 +58,9 @@ _SIGS = {
     "bf_probe_read": (_i32, [_vp, _u64, _u32, _vp, _u64, _vp, _vp]),
     "bf_probe_red": (_i32, [_vp, _u64, _u32, _u32, _vp, _u64, _vp]),
     "bf_probe_rng": (_i32, [_vp, _u64, _u32, _i32, _u32, _u64, _vp]),
+    "bf_probe_gups": (_i32, [_vp, _u64, _u32, _i32, _i32, _u64, _vp]),
+    "bf_set_l2_fetch_granularity": (_i32, [_u32]),
+    "bf_get_l2_fetch_granularity": (_i32, [C.POINTER(_u32)]),
     "bf_set_add_mode": (_i32, [_vp, _i32, _u64, _u64]),
     "bf_get_add_mode": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
     "bf_create_part": (_vp, [_u64, _u32, _u32, _u32, _u32, _u64, _u32, _u32]),
@@ -259,6 +262,20 @@ def bf_probe_red(buf, b: int, block_bits: int, lanes: int, keys, n: int | None =
 
 def bf_probe_rng(buf, b: int, block_bits: int, red: int, lanes: int, n: int, stream=None) -> None:
     _check(_lib.bf_probe_rng(_ptr(buf), b, block_bits, red, lanes, n, _stream(stream)))
+
+
+def bf_probe_gups(buf, nbytes: int, access_bytes: int, red: int, hint: int, n: int, stream=None) -> None:
+    _check(_lib.bf_probe_gups(_ptr(buf), nbytes, access_bytes, red, hint, n, _stream(stream)))
+
+
+def bf_set_l2_fetch_granularity(nbytes: int) -> None:
+    _check(_lib.bf_set_l2_fetch_granularity(nbytes))
+
+
+def bf_get_l2_fetch_granularity() -> int:
+    v = _u32()
+    _check(_lib.bf_get_l2_fetch_granularity(C.byref(v)))
+    return int(v.value)
 
 
 def bf_create_part(m_bits: int, k: int, block_bits: int, word_bits: int, variant: int, seed: int,

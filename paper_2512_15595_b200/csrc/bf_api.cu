@@ -948,4 +948,45 @@ int bf_probe_rng(void* buf, uint64_t b, uint32_t block_bits, int red, uint32_t l
     return check_launch("probe_rng launch");
 }
 
+int bf_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint64_t n, void* stream)
+{
+    if (n == 0) return BF_OK;
+    if (!buf || ((uintptr_t)buf & 63) || nbytes < 64 || (access_bytes != 8 && access_bytes != 32 && access_bytes != 64) ||
+        red < 0 || red > 1 || hint < 0 || hint > 2 || (red && (access_bytes != 8 || hint)) ||
+        (access_bytes == 64 && hint == 2))
+        return fail(BF_EINVAL, "bf_probe_gups: bad arguments");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (launch_probe_gups(buf, nbytes, access_bytes, red, hint, n, (cudaStream_t)stream, 8 * sm_count(dev)))
+        return fail(BF_EINVAL, "bf_probe_gups: unsupported access/hint combination");
+    return check_launch("probe_gups launch");
+}
+
+int bf_set_l2_fetch_granularity(uint32_t bytes)
+{
+    if (bytes != 0 && bytes != 32 && bytes != 64 && bytes != 128)
+        return fail(BF_EINVAL, "L2 fetch granularity must be 0 (driver default), 32, 64 or 128 bytes");
+    static size_t dflt = 0;
+    static bool have_dflt = false;
+    cudaError_t e = cudaSuccess;
+    if (!have_dflt) {
+        if ((e = cudaDeviceGetLimit(&dflt, cudaLimitMaxL2FetchGranularity)) != cudaSuccess)
+            return cuda_fail(e, "cudaDeviceGetLimit(MaxL2FetchGranularity)");
+        have_dflt = true;
+    }
+    if ((e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, bytes ? bytes : dflt)) != cudaSuccess)
+        return cuda_fail(e, "cudaDeviceSetLimit(MaxL2FetchGranularity)");
+    return BF_OK;
+}
+
+int bf_get_l2_fetch_granularity(uint32_t* bytes)
+{
+    if (!bytes) return fail(BF_EINVAL, "null output");
+    size_t v = 0;
+    cudaError_t e = cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetLimit(MaxL2FetchGranularity)");
+    *bytes = (uint32_t)v;
+    return BF_OK;
+}
+
 }  // extern "C"

@@ -258,6 +258,100 @@ __global__ void __launch_bounds__(256) probe_red_rng_kernel(unsigned long long* 
     }
 }
 
+// GUPS-style probes (the paper's random-access speed of light, P:L340
+// footnote: "random 64-bit loads / updates"): every thread keeps
+// MLP independent accesses in flight, addresses uniform over the buffer from
+// an in-register xorshift stream (no key stream, no hashing, no ballot).
+//   read:   BYTES-wide loads (8 = the paper's 64-bit GUPS; 32 / 64 = one
+//           filter block), optional .L2::64B / .L2::128B fill-size hint
+//   update: red.global.or.b64 of one random 8-byte word (1 lane per update)
+template <int BYTES, int HINT>
+__device__ __forceinline__ unsigned long long gups_load(const unsigned long long* p)
+{
+    unsigned long long a, b, c, d;
+    if constexpr (BYTES == 8) {
+        if constexpr (HINT == 1) asm volatile("ld.global.nc.L1::no_allocate.L2::64B.u64 %0, [%1];" : "=l"(a) : "l"(p));
+        else if constexpr (HINT == 2) asm volatile("ld.global.nc.L1::no_allocate.L2::128B.u64 %0, [%1];" : "=l"(a) : "l"(p));
+        else asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(a) : "l"(p));
+        return a;
+    } else {
+        if constexpr (HINT == 1)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];"
+                         : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+        else if constexpr (HINT == 2)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::128B.v4.u64 {%0,%1,%2,%3}, [%4];"
+                         : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+        else
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                         : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+        unsigned long long r = a ^ b ^ c ^ d;
+        if constexpr (BYTES == 64) {
+            if constexpr (HINT == 1)
+                asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];"
+                             : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p + 4));
+            else
+                asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                             : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p + 4));
+            r ^= a ^ b ^ c ^ d;
+        }
+        return r;
+    }
+}
+
+template <int BYTES, int HINT, bool RED, int MLP>
+__global__ void __launch_bounds__(256) probe_gups_kernel(unsigned long long* buf, uint64_t units, uint64_t iters,
+                                                         unsigned long long* sink)
+{
+    constexpr int W = BYTES / 8;  // 64-bit words per access
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t x = mix64(tid + 0x5151ULL) | 1ULL;
+    unsigned long long acc = 0;
+    for (uint64_t it = 0; it < iters; ++it) {
+        unsigned long long v[MLP];
+#pragma unroll
+        for (int j = 0; j < MLP; ++j) {
+            x = xs64(x);
+            const uint64_t u = __umul64hi(x, units);  // uniform over [0, units)
+            if constexpr (RED) red_or(buf + u * W, 1ULL << (x & 63));
+            else v[j] = gups_load<BYTES, HINT>(buf + u * W);
+        }
+        if constexpr (!RED) {
+#pragma unroll
+            for (int j = 0; j < MLP; ++j) acc += v[j];
+        }
+    }
+    if (!RED && acc == 0x9E3779B97F4A7C15ULL) sink[0] = acc;  // keeps the loads alive
+}
+
+int launch_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint64_t n,
+                      cudaStream_t st, int grid)
+{
+    constexpr int MLP = 8;
+    const uint64_t units = nbytes / access_bytes;
+    const uint64_t threads = (uint64_t)grid * 256;
+    const uint64_t iters = (n + threads * MLP - 1) / (threads * MLP);
+    auto* p = (unsigned long long*)buf;
+#define BF_GUPS(B_, H_, R_) probe_gups_kernel<B_, H_, R_, MLP><<<grid, 256, 0, st>>>(p, units, iters, p)
+    if (red) {
+        if (access_bytes != 8) return -1;
+        BF_GUPS(8, 0, true);
+        return 0;
+    }
+    switch (access_bytes * 4 + hint) {
+    case 32: BF_GUPS(8, 0, false); break;
+    case 33: BF_GUPS(8, 1, false); break;
+    case 34: BF_GUPS(8, 2, false); break;
+    case 128: BF_GUPS(32, 0, false); break;
+    case 129: BF_GUPS(32, 1, false); break;
+    case 130: BF_GUPS(32, 2, false); break;
+    case 256: BF_GUPS(64, 0, false); break;
+    case 257: BF_GUPS(64, 1, false); break;
+    default: return -1;
+    }
+#undef BF_GUPS
+    return 0;
+}
+
 // NEXT N4 experiment: the block OR issued by the TMA engine instead of the
 // LSU -- cp.reduce.async.bulk .or.b64 of one B/8-byte block from shared
 // memory per key (one issuing lane per key, every lane of the warp issues).

@@ -34,15 +34,38 @@ def test_bench_json_contract(cuda):
     r = d["roofline"]
     for key in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert key in r, key
-    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    # L2-resident filter: the binding bound is the live L2 random-sector probe
+    assert r["bound"] == "l2" and r["unit"] == "GB/s" and abs(r["frac"] - r["achieved"] / r["peak"]) < 2e-3
+    assert 0 < r["frac"] <= 1.1 and set(d["roofline_kernels"]) == {"add", "contains"}
     assert d["gpu_launches"] >= 2 * d["steps"]
+    n = 1 << 20
+    assert d["config"]["keys_per_step"] == 3 * n and d["fpr"]["negatives"] == n
+    assert 0 < d["fpr"]["measured"] < 0.05
     c = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c)
     e = d["e2e"]
     assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(e)
-    assert e["h2d_bytes_per_step"] == 8 * (1 << 20) and e["unit"] == d["unit"]
+    assert e["h2d_bytes_per_step"] == 8 * 3 * n and e["unit"] == d["unit"]
+    assert e["d2h_bytes_per_step"] == 4 * (2 * n // 32)
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     ref = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c1",
                           "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=600, cwd=ROOT)
     rl = json.loads(ref.stdout.strip().splitlines()[-1])
     assert rl["metric"] == d["metric"] and rl["unit"] == d["unit"] and rl["config"]["workload"] == d["config"]["workload"]
+
+
+def test_bench_default_legs(cuda):
+    """The default line (configs[1] at iso FPR) carries the HBM leg
+    (configs[2] at full size) and the fixed-load leg, each with its own
+    roofline; the measured FPR of the iso leg is within 4 sigma of the
+    exact model."""
+    d = _run("--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e")
+    assert d["config"]["workload"].startswith("configs[1] at iso FPR")
+    assert abs(d["fpr"]["z"]) <= 4
+    assert d["roofline"]["bound"] == "l2"
+    h = d["hbm"]
+    if "skipped" not in h:
+        assert h["workload"].startswith("configs[2]") and h["value"] > 0
+        assert h["roofline_kernels"]["contains"]["bound"] == "hbm"
+        assert h["add_path"] == "binned"
+    assert d["fixed_load"]["workload"].startswith("configs[1] fixed load")

@@ -30,7 +30,7 @@ launches)
   ;;
 prof)
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:bulk_kernel -s 4 -c 2 \
-    -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-probe --no-graph --no-hbm "$@" \
+    -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-probe --no-graph --no-hbm --no-fixed "$@" \
     > gpurun_out/prof_$TAG.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/prof_$TAG.log
   ;;
