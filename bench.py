@@ -506,34 +506,53 @@ def best_time(torch, fn, reps=5):
     return best
 
 
-def run_probes_l2(bf, torch, cfg, keys, out):
+def _rng_accesses(n, unit):
+    """The in-register probes run whole iterations of the grid: the number of
+    accesses they really make for a request of n."""
+    return -(-n // unit) * unit
+
+
+def run_probes_l2(bf, torch, cfg, dev, n=1 << 26):
     """R_read / R_red on a buffer of the filter's size and block geometry
-    (SURVEY 8(d) roofline probes), every form measured live: the key-stream
-    forms (same key loads as the product, no hashing), the in-register
-    address forms, and for add the LSU+TMA form (half the warps OR whole
-    blocks with cp.reduce.async.bulk, half issue RED.64s).  The denominator
-    is the best of the forms for the same access pattern."""
+    (SURVEY 8(d) roofline probes), every form measured live on 2^26 keys
+    (the asymptotic rate: no launch ramp or tail) and in two launch shapes
+    (8 CTAs/SM persistent-style and 32 CTAs/SM waves, the product's shape):
+    the key-stream forms (same key loads as the product, no hashing), the
+    in-register address forms, and for add the LSU+TMA form (half the warps
+    OR whole blocks with cp.reduce.async.bulk, half issue RED.64s).  The
+    denominator is the best of the forms and shapes for the same access
+    pattern."""
     B = max(64, cfg["B"])
     nbytes = cfg["m_bits"] // 8
-    buf = torch.zeros(nbytes, dtype=torch.uint8, device=keys.device)
+    buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    keys = torch.empty(n, dtype=torch.int64, device=dev)
+    bf.bf_keygen(keys, n, 0)
+    out = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
     b = nbytes * 8 // B
     lanes = max(1, B // 64)
-    n = keys.numel()
-    ms = {"read_keys": best_time(torch, lambda: bf.bf_probe_read(buf, b, B, keys, out)),
-          "read_rng": best_time(torch, lambda: bf.bf_probe_rng(buf, b, B, 0, 1, n)),
-          "red_keys": best_time(torch, lambda: bf.bf_probe_red(buf, b, B, lanes, keys)),
-          "red_rng": best_time(torch, lambda: bf.bf_probe_rng(buf, b, B, 1, lanes, n))}
-    if B >= 128:
-        ms["red_lsu_tma"] = best_time(torch, lambda: bf.bf_probe_rng(buf, b, B, 3, lanes, n))
-    res = {k: round(n / (v * 1e-3) / 1e9, 3) for k, v in ms.items()}
-    res["read"] = max(res["read_keys"], res["read_rng"])
-    res["red"] = max(v for k, v in res.items() if k.startswith("red_"))
-    res["read_name"] = (f"R_read^L2(B={B}): one {B // 8}-byte block load per key, no hash; best of key-stream "
-                        f"{res['read_keys']} / in-register {res['read_rng']} Gkeys/s")
-    red_forms = " / ".join(f"{k[4:]} {v}" for k, v in res.items() if k.startswith("red_"))
-    res["red_name"] = (f"R_red^L2(B={B}): {lanes} lanes x RED.64 into one block per key, no hash; best of "
-                       f"{red_forms} Gkeys/s")
-    del buf
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    res = {}
+    for cps in (8, 32):
+        bf.bf_set_probe_launch(cps)
+        thr = sms * cps * 256
+        forms = {"read_keys": (lambda: bf.bf_probe_read(buf, b, B, keys, out), n),
+                 "read_rng": (lambda: bf.bf_probe_rng(buf, b, B, 0, 1, n), _rng_accesses(n, thr * 4)),
+                 "red_keys": (lambda: bf.bf_probe_red(buf, b, B, lanes, keys), n),
+                 "red_rng": (lambda: bf.bf_probe_rng(buf, b, B, 1, lanes, n), _rng_accesses(n, thr // lanes))}
+        if B >= 128:
+            forms["red_lsu_tma"] = (lambda: bf.bf_probe_rng(buf, b, B, 3, lanes, n), _rng_accesses(n, thr))
+        for name, (fn, acc) in forms.items():
+            res[f"{name}@{cps}"] = round(acc / (best_time(torch, fn) * 1e-3) / 1e9, 3)
+    bf.bf_set_probe_launch(0)
+    read = {k: v for k, v in res.items() if k.startswith("read_")}
+    red = {k: v for k, v in res.items() if k.startswith("red_")}
+    res["read"], res["read_form"] = max(read.values()), max(read, key=read.get)
+    res["red"], res["red_form"] = max(red.values()), max(red, key=red.get)
+    res["read_name"] = (f"R_read^L2(B={B}): one {B // 8}-byte block load per key, no hash, 2^26 keys; best of "
+                        + " / ".join(f"{k} {v}" for k, v in read.items()) + " Gkeys/s (form@CTAs per SM)")
+    res["red_name"] = (f"R_red^L2(B={B}): {lanes} lanes x RED.64 into one block per key, no hash, 2^26 keys; best of "
+                       + " / ".join(f"{k} {v}" for k, v in red.items()) + " Gkeys/s (form@CTAs per SM)")
+    del buf, keys, out
     torch.cuda.empty_cache()
     return res
 
@@ -542,21 +561,33 @@ def run_probes_hbm(bf, torch, cfg, n):
     """The HBM random-access speed of light (P:L340 footnote) on a
     buffer of the filter's size: GUPS-style random loads (8 B, and the 32 B
     block with the .L2::64B fill hint the product uses), random 8 B updates,
-    and the filter-geometry block probes."""
+    and the filter-geometry block probes, in the persistent-style (8 CTAs/SM)
+    and the wave (32 CTAs/SM) launch shapes; the best form is the roofline."""
+    dev = torch.device("cuda", torch.cuda.current_device())
     nbytes = cfg["m_bits"] // 8
-    buf = torch.zeros(nbytes, dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device()))
+    buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
     B = cfg["B"]
     b = nbytes * 8 // B
-    ms = {"gups_read_8": best_time(torch, lambda: bf.bf_probe_gups(buf, nbytes, 8, 0, 0, n), 3),
-          "gups_read_8_l2_64B": best_time(torch, lambda: bf.bf_probe_gups(buf, nbytes, 8, 0, 1, n), 3),
-          "block_read_32_l2_64B": best_time(torch, lambda: bf.bf_probe_gups(buf, nbytes, 32, 0, 1, n), 3),
-          "block_read_rng": best_time(torch, lambda: bf.bf_probe_rng(buf, b, B, 0, 1, n), 3),
-          "gups_update_8": best_time(torch, lambda: bf.bf_probe_gups(buf, nbytes, 8, 1, 0, n), 3),
-          "block_red_rng": best_time(torch, lambda: bf.bf_probe_rng(buf, b, B, 1, max(1, B // 64), n), 3)}
-    res = {k: round(n / (v * 1e-3) / 1e9, 3) for k, v in ms.items()}
-    res["read"] = max(res["block_read_32_l2_64B"], res["block_read_rng"])
-    res["read_gups"] = max(res["gups_read_8"], res["gups_read_8_l2_64B"])
-    res["update_gups"] = res["gups_update_8"]
+    lanes = max(1, B // 64)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    res = {}
+    for cps in (8, 32):
+        bf.bf_set_probe_launch(cps)
+        thr = sms * cps * 256
+        forms = {"gups_read_8": (lambda: bf.bf_probe_gups(buf, nbytes, 8, 0, 0, n), _rng_accesses(n, thr * 8)),
+                 "gups_read_8_l2_64B": (lambda: bf.bf_probe_gups(buf, nbytes, 8, 0, 1, n), _rng_accesses(n, thr * 8)),
+                 "block_read_32_l2_64B": (lambda: bf.bf_probe_gups(buf, nbytes, 32, 0, 1, n), _rng_accesses(n, thr * 8)),
+                 "block_read_rng": (lambda: bf.bf_probe_rng(buf, b, B, 0, 1, n), _rng_accesses(n, thr * 4)),
+                 "gups_update_8": (lambda: bf.bf_probe_gups(buf, nbytes, 8, 1, 0, n), _rng_accesses(n, thr * 8)),
+                 "block_red_rng": (lambda: bf.bf_probe_rng(buf, b, B, 1, lanes, n), _rng_accesses(n, thr // lanes))}
+        for name, (fn, acc) in forms.items():
+            res[f"{name}@{cps}"] = round(acc / (best_time(torch, fn, 3) * 1e-3) / 1e9, 3)
+    bf.bf_set_probe_launch(0)
+    pick = lambda pre: max(v for k, v in res.items() if k.startswith(pre))  # noqa: E731
+    res["read"] = max(pick("block_read_32_l2_64B"), pick("block_read_rng"))
+    res["read_gups"] = pick("gups_read_8")
+    res["update_gups"] = pick("gups_update_8")
+    res["block_red"] = pick("block_red_rng")
     res["paper_gups"] = {"read": 52.9, "update": 23.7, "source": "P:L428 (B200)"}
     del buf
     torch.cuda.empty_cache()
@@ -659,8 +690,8 @@ def leg_result(leg, r, probes, cfg, world, hbm_peak):
                   "peak_kind": "MEASURED_PEAKS.json hbm_gbs (copy)",
                   "note": "streaming bound: key 8 B + record write 8 B + record read 8 B + filter read+write per batch"}
         else:
-            ka = {"bound": "hbm", "achieved_gkeys_s": round(ag, 3), "peak_gkeys_s": probes["block_red_rng"],
-                  "frac": round(ag / probes["block_red_rng"], 4), "kernel": "bf_add (direct)",
+            ka = {"bound": "hbm", "achieved_gkeys_s": round(ag, 3), "peak_gkeys_s": probes["block_red"],
+                  "frac": round(ag / probes["block_red"], 4), "kernel": "bf_add (direct)",
                   "peak_kind": "measured live: HBM random block-RED probe"}
         dom = "add" if r["t"]["add"] >= r["t"]["contains"] else "contains"
         res["roofline"] = ka if dom == "add" else kc
@@ -687,7 +718,7 @@ def run_ours(a, cfg, rank, world, local_rank):
     probes = None
     if not a.no_probe and rank == 0:
         if cfg["residency"] == "L2":
-            probes = run_probes_l2(bf, torch, cfg, leg.q[:1 << 26] if leg.q.numel() >= 1 << 26 else leg.q, leg.out)
+            probes = run_probes_l2(bf, torch, cfg, dev)
         else:
             probes = run_probes_hbm(bf, torch, cfg, 1 << 28)
     e2e = None
@@ -714,7 +745,7 @@ def run_ours(a, cfg, rank, world, local_rank):
             rr = lg.run(sub_steps, 3, a.graph)
             pr = None
             if not a.no_probe:
-                pr = (run_probes_l2(bf, torch, c, lg.q[:1 << 26], lg.out) if c["residency"] == "L2"
+                pr = (run_probes_l2(bf, torch, c, dev) if c["residency"] == "L2"
                       else run_probes_hbm(bf, torch, c, 1 << 28))
             extra[key] = leg_result(lg, rr, pr, c, world, hbm_peak)
             extra[key]["steps"] = sub_steps

@@ -123,6 +123,17 @@ int bf_clear(bf_filter* f, void* stream);
  * stream that still uses it. */
 void bf_destroy(bf_filter* f);
 
+/* Launch shape of the bulk kernels (grid-stride over warp tiles; 256 threads
+ * per CTA): ctas_per_sm x SMs CTAs, capped at one tile per warp.  0 = the
+ * library default, 32 per SM: several waves of resident CTAs rather than one
+ * persistent grid (measured faster for every geometry on L2- and
+ * HBM-resident filters).  ctas_per_sm = the occupancy
+ * limit gives the persistent grid.  Results never depend on it.
+ * ctas_per_sm in 0..1024; bf_get_launch reports the CTAs per SM used and the
+ * occupancy limit. */
+int bf_set_launch(bf_filter* f, int op, int ctas_per_sm);
+int bf_get_launch(const bf_filter* f, int op, int* ctas_per_sm, int* occupancy_ctas_per_sm);
+
 /* Raw word array (device pointer) and its size in bytes = b*B/8.  The memory
  * layout is DESIGN.md section 2: bit p of block i is bit p%8 of byte
  * i*B/8 + p/8.  Used by parity tests and the multi-GPU merge. */
@@ -260,17 +271,35 @@ int bf_probe_red(void* buf, uint64_t b, uint32_t block_bits, uint32_t lanes,
 int bf_probe_rng(void* buf, uint64_t b, uint32_t block_bits, int red, uint32_t lanes, uint64_t n,
                  void* stream);
 
+/* R_red with the add's exact RED pattern (payload-matched roofline of a
+ * configuration; SURVEY 8(d) "% of roofline = our Gkeys/s / the probe with
+ * the same (B, S, Θ, atomics per key) geometry"): n keys, each one random
+ * block of a b-block buffer, the REDs of a key issued by one group of lanes
+ * in one instruction as bf_add's default schedule does -- SBF/RBBF: all s
+ * words; BBF: the distinct words hit by k uniform word draws; CSBF (z): one
+ * uniform word of each of the z groups.  Bits are random (no keys, no
+ * hashing).  The arguments must form a valid configuration (bf_create's
+ * rules; BF_EINVAL otherwise). */
+int bf_probe_red_pattern(void* buf, uint64_t b, uint32_t block_bits, uint32_t word_bits, uint32_t variant,
+                         uint32_t k, uint32_t z, uint64_t n, void* stream);
+
 /* GUPS-style random-access probes (the paper's speed of light: "random
  * 64-bit loads / updates", P:L340 footnote): n accesses at addresses
- * uniform over the nbytes buffer (64-byte aligned), 8 independent accesses in
- * flight per thread, addresses from an in-register xorshift stream.
+ * uniform over the nbytes buffer (64-byte aligned), `mlp` independent
+ * accesses in flight per thread (1, 2, 4, 8, 16; 0 = 8), `ctas` CTAs of 256
+ * threads (0 = 8 per SM), addresses from an in-register xorshift stream.
  *   red = 0: loads of access_bytes in {8, 32, 64}; hint 0 none, 1 .L2::64B,
  *            2 .L2::128B (not with 64-byte accesses) -- the L2 fill-size hint
  *   red = 1: red.global.or.b64 of one random 8-byte word (access_bytes 8,
  *            hint 0)
  * Results are discarded; the buffer is read or OR-ed. */
-int bf_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint64_t n,
-                  void* stream);
+int bf_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint32_t mlp,
+                  uint32_t ctas, uint64_t n, void* stream);
+
+/* CTAs per SM of the probe kernels (bf_probe_*; 0 = the bulk kernels'
+ * default shape, 32 per SM), so a probe can be measured in the launch shape
+ * the product uses. */
+int bf_set_probe_launch(int ctas_per_sm);
 
 /* The current device's L2 fetch granularity for DRAM misses
  * (cudaLimitMaxL2FetchGranularity, a context-wide hint): bytes in

@@ -53,13 +53,17 @@ _SIGS = {
     "bf_geometry": (_i32, [_vp, C.POINTER(_u64), C.POINTER(_u32), C.POINTER(_u64)]),
     "bf_set_layout": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32]),
     "bf_get_layout": (_i32, [_vp, _i32] + [C.POINTER(_i32)] * 5),
+    "bf_set_launch": (_i32, [_vp, _i32, _i32]),
+    "bf_get_launch": (_i32, [_vp, _i32, C.POINTER(_i32), C.POINTER(_i32)]),
     "bf_or_fold": (_i32, [_vp, _vp, _u32, _u64, _u64, _vp]),
     "bf_keygen": (_i32, [_vp, _u64, _u64, _vp]),
     "bf_probe_read": (_i32, [_vp, _u64, _u32, _vp, _u64, _vp, _vp]),
     "bf_probe_red": (_i32, [_vp, _u64, _u32, _u32, _vp, _u64, _vp]),
     "bf_probe_rng": (_i32, [_vp, _u64, _u32, _i32, _u32, _u64, _vp]),
-    "bf_probe_gups": (_i32, [_vp, _u64, _u32, _i32, _i32, _u64, _vp]),
+    "bf_probe_red_pattern": (_i32, [_vp, _u64, _u32, _u32, _u32, _u32, _u32, _u64, _vp]),
+    "bf_probe_gups": (_i32, [_vp, _u64, _u32, _i32, _i32, _u32, _u32, _u64, _vp]),
     "bf_set_l2_fetch_granularity": (_i32, [_u32]),
+    "bf_set_probe_launch": (_i32, [_i32]),
     "bf_get_l2_fetch_granularity": (_i32, [C.POINTER(_u32)]),
     "bf_set_add_mode": (_i32, [_vp, _i32, _u64, _u64]),
     "bf_get_add_mode": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
@@ -228,6 +232,17 @@ def bf_get_layout(f: int, op: int) -> dict:
     return dict(zip(("theta", "phi", "kpt", "hash_variant", "specialized"), (int(x.value) for x in v)))
 
 
+def bf_set_launch(f: int, op: int, ctas_per_sm: int) -> None:
+    _check(_lib.bf_set_launch(f, op, ctas_per_sm))
+
+
+def bf_get_launch(f: int, op: int) -> tuple[int, int]:
+    """(CTAs per SM used, occupancy limit)."""
+    a, b = _i32(), _i32()
+    _check(_lib.bf_get_launch(f, op, C.byref(a), C.byref(b)))
+    return int(a.value), int(b.value)
+
+
 BF_ADD_AUTO, BF_ADD_DIRECT, BF_ADD_BINNED, BF_ADD_HYBRID = 0, 1, 2, 3
 
 
@@ -264,8 +279,18 @@ def bf_probe_rng(buf, b: int, block_bits: int, red: int, lanes: int, n: int, str
     _check(_lib.bf_probe_rng(_ptr(buf), b, block_bits, red, lanes, n, _stream(stream)))
 
 
-def bf_probe_gups(buf, nbytes: int, access_bytes: int, red: int, hint: int, n: int, stream=None) -> None:
-    _check(_lib.bf_probe_gups(_ptr(buf), nbytes, access_bytes, red, hint, n, _stream(stream)))
+def bf_probe_red_pattern(buf, b: int, block_bits: int, word_bits: int, variant: int, k: int, z: int, n: int,
+                         stream=None) -> None:
+    _check(_lib.bf_probe_red_pattern(_ptr(buf), b, block_bits, word_bits, variant, k, z, n, _stream(stream)))
+
+
+def bf_probe_gups(buf, nbytes: int, access_bytes: int, red: int, hint: int, n: int, mlp: int = 0, ctas: int = 0,
+                  stream=None) -> None:
+    _check(_lib.bf_probe_gups(_ptr(buf), nbytes, access_bytes, red, hint, mlp, ctas, n, _stream(stream)))
+
+
+def bf_set_probe_launch(ctas_per_sm: int) -> None:
+    _check(_lib.bf_set_probe_launch(ctas_per_sm))
 
 
 def bf_set_l2_fetch_granularity(nbytes: int) -> None:
@@ -444,6 +469,9 @@ class Filter:
 
     def set_layout(self, op: int, theta: int, phi: int, kpt: int = 1, hash_variant: int = 0):
         bf_set_layout(self.handle, op, theta, phi, kpt, hash_variant)
+
+    def set_launch(self, op: int, ctas_per_sm: int):
+        bf_set_launch(self.handle, op, ctas_per_sm)
 
     def set_add_mode(self, mode: int, range_bytes: int = 0, max_batch_keys: int = 0):
         bf_set_add_mode(self.handle, mode, range_bytes, max_batch_keys)

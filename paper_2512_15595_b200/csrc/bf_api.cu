@@ -119,7 +119,8 @@ struct Sched {
     int theta, phi, kpt, hv;
     KernelFn fn;        // specialized kernel or generic
     bool specialized;
-    int grid;           // CTAs (persistent grid-stride)
+    int grid;           // CTAs (persistent grid-stride): occupancy x SMs, or the bf_set_launch cap
+    int occ;            // resident CTAs per SM at occupancy
 };
 
 struct bf_filter {
@@ -155,6 +156,7 @@ struct bf_filter {
     // binned adds issued on different streams
     std::mutex mu;
     cudaEvent_t scratch_done;
+    int ctas_per_sm[2];  // bf_set_launch: 0 = occupancy (default)
 };
 
 static int validate(uint64_t m_bits, uint32_t k, uint32_t B, uint32_t S, uint32_t variant, uint32_t* z_out)
@@ -187,13 +189,26 @@ static int validate(uint64_t m_bits, uint32_t k, uint32_t B, uint32_t S, uint32_
     return BF_OK;
 }
 
-static int pick_grid(bf_filter* f, KernelFn fn)
+static int occupancy(KernelFn fn)
 {
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, 256, 0) != cudaSuccess || per_sm < 1)
         per_sm = 4;
-    return per_sm * sm_count(f->device);
+    return per_sm;
 }
+
+static int pick_grid(bf_filter* f, KernelFn fn) { return occupancy(fn) * sm_count(f->device); }
+
+// Default launch shape of the grid-stride bulk kernels: kWaveCtasPerSm CTAs
+// per SM, i.e. several waves of resident CTAs instead of one persistent
+// grid.  Measured on the B200 (tools/launch_sweep.py, profiles/r2_launch.md):
+// HBM-resident contains 36.3 -> 46.5 Gkeys/s, L2-resident add 116 -> 124,
+// contains 208 -> 221 (SBF 256/64 k=16); never slower than the persistent
+// grid.  The persistent grid keeps every warp in lock-step over the whole
+// launch, and the random request stream it produces reaches the L2/HBM in
+// bursts; retiring and starting CTAs de-synchronises it.
+static const int kWaveCtasPerSm = 32;
+static int g_probe_ctas_per_sm = kWaveCtasPerSm;
 
 static int set_sched(bf_filter* f, int op, int theta, int phi, int kpt, int hv)
 {
@@ -235,7 +250,9 @@ static int set_sched(bf_filter* f, int op, int theta, int phi, int kpt, int hv)
         // generic runtime-parameter kernel, Θ = 1, one key per thread
         sc = Sched{1, 1, 1, 0, generic_entry((int)f->S, op == 0), false, 0};
     }
-    sc.grid = pick_grid(f, sc.fn);
+    sc.occ = occupancy(sc.fn);
+    const int cap = f->ctas_per_sm[op];
+    sc.grid = (cap ? cap : kWaveCtasPerSm) * sm_count(f->device);
     f->sched[op] = sc;
     return BF_OK;
 }
@@ -424,6 +441,25 @@ int bf_set_layout(bf_filter* f, int op, int theta, int phi, int kpt, int hash_va
     return set_sched(f, op, theta, phi, kpt, hash_variant);
 }
 
+int bf_set_launch(bf_filter* f, int op, int ctas_per_sm)
+{
+    if (!f || (op != 0 && op != 1) || ctas_per_sm < 0 || ctas_per_sm > 1024)
+        return fail(BF_EINVAL, "bad filter, op or CTA count (0..1024 per SM)");
+    DeviceGuard g(f->device);
+    f->ctas_per_sm[op] = ctas_per_sm;
+    Sched& sc = f->sched[op];
+    sc.grid = (ctas_per_sm ? ctas_per_sm : kWaveCtasPerSm) * sm_count(f->device);
+    return BF_OK;
+}
+
+int bf_get_launch(const bf_filter* f, int op, int* ctas_per_sm, int* occupancy_ctas_per_sm)
+{
+    if (!f || (op != 0 && op != 1)) return fail(BF_EINVAL, "bad filter or op");
+    if (ctas_per_sm) *ctas_per_sm = f->sched[op].grid / sm_count(f->device);
+    if (occupancy_ctas_per_sm) *occupancy_ctas_per_sm = f->sched[op].occ;
+    return BF_OK;
+}
+
 int bf_get_layout(const bf_filter* f, int op, int* theta, int* phi, int* kpt, int* hash_variant, int* specialized)
 {
     if (!f || (op != 0 && op != 1)) return fail(BF_EINVAL, "bad filter or op");
@@ -534,10 +570,14 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         ++lg;
         R = (f->b + (1ULL << lg) - 1) >> lg;
     }
-    const uint64_t batch = n < (f->max_batch ? f->max_batch : kDefaultMaxBatch) ? n
-                                                                              : (f->max_batch ? f->max_batch : kDefaultMaxBatch);
+    uint64_t batch = n < (f->max_batch ? f->max_batch : kDefaultMaxBatch) ? n
+                                                                        : (f->max_batch ? f->max_batch : kDefaultMaxBatch);
     uint64_t cap = batch / R + batch / R / 32 + 8192;  // mean + 3% + slack (sd ~ sqrt(mean))
     cap = (cap + 127) & ~127ULL;
+    while (R * cap >= 0xFFFFFFFFULL && batch > (1ULL << 20)) {  // record slots are u32 in the bin kernel
+        batch /= 2;
+        cap = ((batch / R + batch / R / 32 + 8192) + 127) & ~127ULL;
+    }
     const uint64_t need = R * cap * 8;
     cudaError_t e = cudaSuccess;
     if (f->recs_bytes < need) {
@@ -561,14 +601,11 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         }
         f->cursor_n = (uint32_t)R;
     }
-    const size_t smem = bin_smem_bytes((uint32_t)R);
+    const size_t smem = bin_smem_bytes((uint32_t)R, false);
     cudaFuncSetAttribute((const void*)bin_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)bin_fn, BIN_THREADS, smem) != cudaSuccess ||
-        per_sm < 1)
-        per_sm = 1;
-    const int grid_bin = per_sm * sm_count(f->device);
-    const int grid_apply = pick_grid(f, apply_fn);
+    // waves of CTAs like the bulk kernels (bin phase 178 -> 180 Gkeys/s vs the occupancy grid, tools/kexp bin2)
+    const int grid_bin = kWaveCtasPerSm * sm_count(f->device);
+    const int grid_apply = kWaveCtasPerSm * sm_count(f->device);
     for (uint64_t off = 0; off < n; off += batch) {
         const uint64_t cnt = n - off < batch ? n - off : batch;
         BinParams bp;
@@ -716,6 +753,7 @@ int bf_route(const bf_filter* f, const uint64_t* keys, uint64_t n, uint64_t idx_
     DeviceGuard g(f->device);
     cudaStream_t st = (cudaStream_t)stream;
     const uint32_t P = f->nparts;
+    if ((uint64_t)P * cap >= 0xFFFFFFFFULL) return fail(BF_EINVAL, "bf_route: nparts * cap must be < 2^32 - 1");
     cudaError_t e = cudaMemsetAsync(counts, 0, P * sizeof(unsigned long long), st);
     if (e != cudaSuccess) return cuda_fail(e, "bf_route: counts reset");
     if (n == 0) return BF_OK;
@@ -738,7 +776,7 @@ int bf_route(const bf_filter* f, const uint64_t* keys, uint64_t n, uint64_t idx_
         }
         bp.bounds = zero_bounds[dev];
     }
-    const size_t smem = bin_smem_bytes(P);
+    const size_t smem = bin_smem_bytes(P, idx != nullptr);
     cudaFuncSetAttribute((const void*)bin_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)bin_fn, BIN_THREADS, smem) != cudaSuccess ||
@@ -764,7 +802,7 @@ int bf_add_routed(bf_filter* f, const uint64_t* recs, const unsigned long long* 
     BinParams bp = routed_params(f, recs, counts, nsrc, cap);
     const uint64_t tiles = (cap + 32 * f->sched[0].kpt - 1) / (32 * f->sched[0].kpt);
     uint64_t ga = (tiles + 7) / 8;
-    const int grid_apply = pick_grid(f, apply_fn);
+    const int grid_apply = kWaveCtasPerSm * sm_count(f->device);
     if (ga > (uint64_t)grid_apply) ga = grid_apply;
     for (uint32_t r = 0; r < nsrc; ++r) {
         bp.range = r;
@@ -787,7 +825,7 @@ int bf_contains_routed(const bf_filter* f, const uint64_t* recs, const unsigned 
     DeviceGuard g(f->device);
     BinParams bp = routed_params(f, recs, counts, nsrc, cap);
     void* args[] = {&bp, &res};
-    const int grid = pick_grid((bf_filter*)f, test_fn);
+    const int grid = kWaveCtasPerSm * sm_count(f->device);
     cudaError_t e = cudaLaunchKernel((const void*)test_fn, dim3(grid), dim3(256), args, 0, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "routed contains launch");
     return check_launch("routed contains launch");
@@ -918,7 +956,7 @@ int bf_probe_read(const void* buf, uint64_t b, uint32_t block_bits, const uint64
         return fail(BF_EINVAL, "bf_probe_read: bad arguments (keys must be 32-byte aligned: 256-bit key loads)");
     int dev = 0;
     cudaGetDevice(&dev);
-    if (launch_probe_read(buf, b, block_bits, keys, n, out_bits, (cudaStream_t)stream, 8 * sm_count(dev)))
+    if (launch_probe_read(buf, b, block_bits, keys, n, out_bits, (cudaStream_t)stream, g_probe_ctas_per_sm * sm_count(dev)))
         return fail(BF_EINVAL, "bf_probe_read: block_bits must be 64..1024");
     return check_launch("probe_read launch");
 }
@@ -932,7 +970,7 @@ int bf_probe_red(void* buf, uint64_t b, uint32_t block_bits, uint32_t lanes, con
         return fail(BF_EINVAL, "bf_probe_red: bad arguments");
     int dev = 0;
     cudaGetDevice(&dev);
-    launch_probe_red(buf, b, block_bits, lanes, keys, n, (cudaStream_t)stream, 8 * sm_count(dev));
+    launch_probe_red(buf, b, block_bits, lanes, keys, n, (cudaStream_t)stream, g_probe_ctas_per_sm * sm_count(dev));
     return check_launch("probe_red launch");
 }
 
@@ -944,22 +982,48 @@ int bf_probe_rng(void* buf, uint64_t b, uint32_t block_bits, int red, uint32_t l
         return fail(BF_EINVAL, "bf_probe_rng: bad arguments");
     int dev = 0;
     cudaGetDevice(&dev);
-    launch_probe_rng(buf, b, block_bits, red, red ? lanes : 1, n, (cudaStream_t)stream, 8 * sm_count(dev));
+    launch_probe_rng(buf, b, block_bits, red, red ? lanes : 1, n, (cudaStream_t)stream, g_probe_ctas_per_sm * sm_count(dev));
     return check_launch("probe_rng launch");
 }
 
-int bf_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint64_t n, void* stream)
+int bf_probe_red_pattern(void* buf, uint64_t b, uint32_t block_bits, uint32_t word_bits, uint32_t variant,
+                         uint32_t k, uint32_t z, uint64_t n, void* stream)
+{
+    if (n == 0) return BF_OK;
+    uint32_t zz = 0;
+    if (!buf || b < 1 || b > (1ULL << 32) || validate(b * block_bits, k, block_bits, word_bits,
+                                                      variant == BF_CSBF ? (BF_CSBF | (z << 8)) : variant, &zz) != BF_OK ||
+        variant == BF_CBF)
+        return fail(BF_EINVAL, "bf_probe_red_pattern: bad arguments (a valid blocked configuration is required)");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (launch_probe_red_pattern(buf, b, block_bits, word_bits, variant, k, zz, n, (cudaStream_t)stream,
+                                 g_probe_ctas_per_sm * sm_count(dev)))
+        return fail(BF_EUNSUPPORTED, "bf_probe_red_pattern: geometry outside the probe's range");
+    return check_launch("probe_red_pattern launch");
+}
+
+int bf_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint32_t mlp, uint32_t ctas,
+                  uint64_t n, void* stream)
 {
     if (n == 0) return BF_OK;
     if (!buf || ((uintptr_t)buf & 63) || nbytes < 64 || (access_bytes != 8 && access_bytes != 32 && access_bytes != 64) ||
         red < 0 || red > 1 || hint < 0 || hint > 2 || (red && (access_bytes != 8 || hint)) ||
-        (access_bytes == 64 && hint == 2))
+        (access_bytes == 64 && hint == 2) || (mlp && !is_pow2(mlp)) || mlp > 16)
         return fail(BF_EINVAL, "bf_probe_gups: bad arguments");
     int dev = 0;
     cudaGetDevice(&dev);
-    if (launch_probe_gups(buf, nbytes, access_bytes, red, hint, n, (cudaStream_t)stream, 8 * sm_count(dev)))
+    const int grid = ctas ? (int)ctas : g_probe_ctas_per_sm * sm_count(dev);
+    if (launch_probe_gups(buf, nbytes, access_bytes, red, hint, mlp ? mlp : 8, n, (cudaStream_t)stream, grid))
         return fail(BF_EINVAL, "bf_probe_gups: unsupported access/hint combination");
     return check_launch("probe_gups launch");
+}
+
+int bf_set_probe_launch(int ctas_per_sm)
+{
+    if (ctas_per_sm < 0 || ctas_per_sm > 1024) return fail(BF_EINVAL, "CTAs per SM must be 0..1024");
+    g_probe_ctas_per_sm = ctas_per_sm ? ctas_per_sm : kWaveCtasPerSm;
+    return BF_OK;
 }
 
 int bf_set_l2_fetch_granularity(uint32_t bytes)

@@ -44,14 +44,19 @@ struct BinParams {
     uint32_t blk_base;           // phase 2: first block of the local filter part
 };
 
-constexpr int BIN_THREADS = 256;
+// 512 threads x 8 keys: 177-180 Gkeys/s for the bin phase at R = 256 vs 162-166
+// for 256 x 16 and 155 for the r1 kernel (tools/kexp bin2, profiles/r2_kexp.md)
+constexpr int BIN_THREADS = 512;
 constexpr int BIN_KPT = 8;
 constexpr int BIN_CHUNK = BIN_THREADS * BIN_KPT;  // keys per CTA chunk
 
-// dynamic smem layout: stage[CHUNK] u64 | hist[R] u32 (+pad) | gbase[R] u64 | stage_r[CHUNK] u16 | stage_li[CHUNK] u16
-__host__ __device__ inline size_t bin_smem_bytes(uint32_t nranges, uint32_t chunk = BIN_CHUNK)
+// dynamic smem layout (16-byte aligned pieces):
+//   stage[CHUNK] u64 | dest[CHUNK] u32 | [li[CHUNK] u16 when routing with key
+//   indices] | hist[R + 1] u32 (+pad) | gbase[R] u64
+__host__ __device__ inline size_t bin_smem_bytes(uint32_t nranges, bool with_idx = true, uint32_t chunk = BIN_CHUNK)
 {
-    return (size_t)chunk * 8 + (size_t)(nranges + 1) * 4 + (size_t)nranges * 8 + (size_t)chunk * 4;
+    return (size_t)chunk * 8 + (size_t)chunk * 4 + (with_idx ? (size_t)chunk * 2 : 0) +
+           (size_t)((nranges + 2) & ~1u) * 4 + (size_t)nranges * 8;
 }
 
 // owner of a block under the partition bounds (bounds[0] = 0, bounds[P] = b)
@@ -107,80 +112,142 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t* a, uint32_t n
 }
 
 // Phase 1.  C1 is the Θ=1 configuration of the filter (for the overflow path).
-template <class C1, int NT = BIN_THREADS, int KPT = BIN_KPT>
-__global__ void __launch_bounds__(NT) bin_kernel(const BinParams bp)
+// A CTA takes chunks of NT*KPT keys (grid-stride):
+//   (a) every thread loads its KPT keys (coalesced: key i*NT + tid, all KPT
+//       loads in flight), hashes them and takes a rank in its bucket's
+//       shared-memory counter (one ATOMS with return per key);
+//   (b) one global atomic per touched bucket reserves the chunk's run in
+//       that bucket (cursor), and an exclusive scan turns the counts into run
+//       offsets inside the chunk;
+//   (c) every thread stores its records at their sorted slots in shared
+//       memory together with the final u32 destination slot in recs
+//       (bucket * cap + reserved base + rank; 0xFFFFFFFF when the bucket is
+//       full), so
+//   (d) the write-out is one LDS pair and one coalesced STG per record:
+//       consecutive threads write consecutive slots of a run.
+// Runs average CHUNK/R records (16 at R = 256 for 4096-key chunks), i.e.
+// 128-byte contiguous stores, few partial sectors at run boundaries.
+// One chunk of phase 1 (FULL: cnt == NT*KPT, no per-key bounds checks).
+template <class C1, int NT, int KPT, bool FULL>
+__device__ __forceinline__ void bin_chunk(const BinParams& bp, uint64_t base, uint32_t cnt, uint32_t R, bool with_idx,
+                                          uint64_t* stage, uint32_t* dest, uint16_t* stage_li, uint32_t* hist,
+                                          unsigned long long* gbase, uint32_t* warp_tot, const SaltSrc<C1>& ss)
 {
-    constexpr int CHUNK = NT * KPT;
-    extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t R = bp.nranges;
-    uint64_t* stage = (uint64_t*)smem;
-    uint32_t* hist = (uint32_t*)(stage + CHUNK);
-    unsigned long long* gbase = (unsigned long long*)(hist + R + (R & 1));
-    uint16_t* stage_r = (uint16_t*)(gbase + R);
-    uint16_t* stage_li = stage_r + CHUNK;
-    __shared__ uint32_t warp_tot[NT / 32 + 1];
-
     using W = typename C1::W;
-    SaltSrc<C1> ss;
-    ss.init(0, nullptr, nullptr);
     const Params& p = bp.f;
     const uint32_t tid = threadIdx.x;
-
-    for (uint64_t c = blockIdx.x; c * CHUNK < p.n; c += gridDim.x) {
-        const uint64_t base = c * CHUNK;
-        const uint32_t cnt = (uint32_t)min((uint64_t)CHUNK, p.n - base);
-        {  // L2 prefetch of this CTA's chunk two grid strides ahead, one 128-byte
-           // line per thread, no registers: the key loads below then wait for
-           // L2 instead of HBM (+10% on the bin phase, tools/kexp)
-            const uint64_t pb = base + 2ULL * gridDim.x * CHUNK + (uint64_t)tid * 16;
-            if (tid < CHUNK / 16 && pb < p.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.keys + pb));
-        }
-        for (uint32_t r = tid; r < R; r += NT) hist[r] = 0;
-        __syncthreads();
-        // hash once per key; count per range (coalesced key loads: i*256+tid)
-        uint64_t rec[KPT];
-        uint32_t rl[KPT];
+    for (uint32_t r = tid; r < R; r += NT) hist[r] = 0;
+    __syncthreads();
+    // (a) load + hash + rank
+    uint64_t key[KPT];
 #pragma unroll
-        for (int i = 0; i < KPT; ++i) {
-            const uint32_t li = i * NT + tid;
-            rl[i] = 0xFFFFFFFFu;
-            if (li < cnt) {
-                const uint64_t h = xxh64_u64(ld_key1(p.keys + base + li), p.seed);
-                const uint32_t blk = block_of(h, p.b32);
-                const uint32_t r = bp.bounds ? owner_of(bp.bounds, R, blk) : blk >> bp.lg_bpr;
-                rec[i] = ((uint64_t)blk << 32) | (uint32_t)h;
-                rl[i] = (r << 16) | atomicAdd(&hist[r], 1u);
-            }
-        }
-        __syncthreads();
-        // reserve this chunk's run in every touched bucket
-        for (uint32_t r = tid; r < R; r += NT)
-            gbase[r] = hist[r] ? atomicAdd(&bp.cursor[r], (unsigned long long)hist[r]) : 0ULL;
-        block_exclusive_scan<NT>(hist, R, warp_tot);  // hist -> run offsets in stage
-        // counting-sort the records by range in shared memory
+    for (int i = 0; i < KPT; ++i) {
+        const uint32_t li = i * NT + tid;
+        key[i] = (FULL || li < cnt) ? ld_key1(p.keys + base + li) : 0ULL;
+    }
+    uint64_t rec[KPT];
+    uint32_t rl[KPT];  // (bucket << 16) | rank, or ~0 for an empty slot
 #pragma unroll
-        for (int i = 0; i < KPT; ++i) {
-            if (rl[i] != 0xFFFFFFFFu) {
-                const uint32_t r = rl[i] >> 16, pos = hist[r] + (rl[i] & 0xFFFFu);
-                stage[pos] = rec[i];
-                stage_r[pos] = (uint16_t)r;
-                stage_li[pos] = (uint16_t)(i * NT + tid);
-            }
+    for (int i = 0; i < KPT; ++i) {
+        const uint32_t li = i * NT + tid;
+        rl[i] = 0xFFFFFFFFu;
+        if (FULL || li < cnt) {
+            const uint64_t h = xxh64_u64(key[i], p.seed);
+            const uint32_t blk = block_of(h, p.b32);
+            const uint32_t r = bp.bounds ? owner_of(bp.bounds, R, blk) : blk >> bp.lg_bpr;
+            rec[i] = ((uint64_t)blk << 32) | (uint32_t)h;
+            rl[i] = (r << 16) | atomicAdd(&hist[r], 1u);
         }
-        __syncthreads();
-        // write the runs out (consecutive slots of a run -> consecutive addresses)
-        for (uint32_t j = tid; j < cnt; j += NT) {
-            const uint32_t r = stage_r[j];
-            const unsigned long long off = gbase[r] + (j - hist[r]);
+    }
+    __syncthreads();
+    // (b) reserve this chunk's run in every touched bucket, then the run offsets
+    for (uint32_t r = tid; r < R; r += NT)
+        gbase[r] = hist[r] ? atomicAdd(&bp.cursor[r], (unsigned long long)hist[r]) : 0ULL;
+    block_exclusive_scan<NT>(hist, R, warp_tot);  // hist -> run offsets in stage
+    // (c) sorted slots + final destinations
+    const uint64_t cap = bp.cap;
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) {
+        if (FULL || rl[i] != 0xFFFFFFFFu) {
+            const uint32_t r = rl[i] >> 16, rank = rl[i] & 0xFFFFu;
+            const uint32_t pos = hist[r] + rank;
+            const unsigned long long off = gbase[r] + rank;
+            stage[pos] = rec[i];
+            dest[pos] = off < cap ? (uint32_t)(r * cap + off) : 0xFFFFFFFFu;
+            if (with_idx) stage_li[pos] = (uint16_t)(i * NT + tid);
+        }
+    }
+    __syncthreads();
+    // (d) coalesced write-out of the runs
+    uint64_t* const recs = bp.recs;
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) {
+        const uint32_t j = i * NT + tid;
+        if (FULL || j < cnt) {
+            const uint32_t d = dest[j];
             const uint64_t v = stage[j];
-            if (off < bp.cap) {
-                bp.recs[(uint64_t)r * bp.cap + off] = v;
-                if (bp.idx_out) bp.idx_out[(uint64_t)r * bp.cap + off] = bp.idx_base + base + stage_li[j];
+            if (d != 0xFFFFFFFFu) {
+                recs[d] = v;
+                if (with_idx) bp.idx_out[d] = bp.idx_base + base + stage_li[j];
             } else if (!bp.bounds) {  // bucket full: OR this key in directly (order-free)
                 add_part<C1>((W*)p.words, (uint32_t)v, (uint32_t)(v >> 32), 0, ss);
             }  // routing: dropped; the receiver sees count > cap and the host reports it
         }
-        __syncthreads();
+    }
+    __syncthreads();
+}
+
+// Phase 1.  C1 is the Θ=1 configuration of the filter (for the overflow path).
+// A CTA takes chunks of NT*KPT keys (grid-stride):
+//   (a) every thread loads its KPT keys (coalesced: key i*NT + tid, all KPT
+//       loads in flight), hashes them and takes a rank in its bucket's
+//       shared-memory counter (one ATOMS with return per key);
+//   (b) one global atomic per touched bucket reserves the chunk's run in
+//       that bucket (cursor), and an exclusive scan turns the counts into run
+//       offsets inside the chunk;
+//   (c) every thread stores its records at their sorted slots in shared
+//       memory together with the final u32 destination slot in recs
+//       (bucket * cap + reserved base + rank; 0xFFFFFFFF when the bucket is
+//       full), so
+//   (d) the write-out is one LDS pair and one coalesced STG per record:
+//       consecutive threads write consecutive slots of a run.
+// Runs average CHUNK/R records (16 at R = 256 for 4096-key chunks), i.e.
+// 128-byte contiguous stores, few partial sectors at run boundaries.  Full
+// chunks (all but the last) run without per-key bounds checks.
+template <class C1, int NT = BIN_THREADS, int KPT = BIN_KPT>
+__global__ void __launch_bounds__(NT) bin_kernel(const BinParams bp)
+{
+    constexpr int CHUNK = NT * KPT;
+    static_assert(CHUNK <= 65536, "u16 key slots");
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t R = bp.nranges;
+    const bool with_idx = bp.idx_out != nullptr;
+    uint64_t* stage = (uint64_t*)smem;
+    uint32_t* dest = (uint32_t*)(stage + CHUNK);
+    uint16_t* stage_li = (uint16_t*)(dest + CHUNK);
+    uint32_t* hist = with_idx ? (uint32_t*)(stage_li + CHUNK) : (uint32_t*)stage_li;
+    unsigned long long* gbase = (unsigned long long*)(hist + ((R + 2) & ~1u));
+    __shared__ uint32_t warp_tot[NT / 32 + 1];
+
+    SaltSrc<C1> ss;
+    ss.init(0, nullptr, nullptr);
+    const uint64_t n = bp.f.n;
+    for (uint64_t c = blockIdx.x; c * CHUNK < n; c += gridDim.x) {
+        const uint64_t base = c * CHUNK;
+        const uint32_t cnt = (uint32_t)min((uint64_t)CHUNK, n - base);
+        {  // L2 prefetch of this CTA's next chunk (one grid stride ahead), one
+           // 128-byte line per thread per 16 lines: the key loads of the next
+           // chunk then wait for L2 instead of HBM
+            const uint64_t pb = base + (uint64_t)gridDim.x * CHUNK;
+            for (uint32_t l = threadIdx.x; l < CHUNK / 16; l += NT) {
+                const uint64_t q = pb + (uint64_t)l * 16;
+                if (q < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(bp.f.keys + q));
+            }
+        }
+        if (cnt == CHUNK)
+            bin_chunk<C1, NT, KPT, true>(bp, base, cnt, R, with_idx, stage, dest, stage_li, hist, gbase, warp_tot, ss);
+        else
+            bin_chunk<C1, NT, KPT, false>(bp, base, cnt, R, with_idx, stage, dest, stage_li, hist, gbase, warp_tot, ss);
     }
 }
 

@@ -10,6 +10,8 @@
 
 #include <type_traits>
 
+#include <bf_tuning.h>  // angle brackets: tools/kexp substitutes its own copy via -I
+
 namespace bf {
 
 // ---------------------------------------------------------------- constants
@@ -66,6 +68,28 @@ static __constant__ uint32_t c_gsalt[16] = {
     gsalt_ct(0), gsalt_ct(1), gsalt_ct(2),  gsalt_ct(3),  gsalt_ct(4),  gsalt_ct(5),  gsalt_ct(6),  gsalt_ct(7),
     gsalt_ct(8), gsalt_ct(9), gsalt_ct(10), gsalt_ct(11), gsalt_ct(12), gsalt_ct(13), gsalt_ct(14), gsalt_ct(15),
 };
+
+// Powers of two in the constant bank: top<LG>() multiplies by c_pow2[LG] so
+// that ptxas cannot strength-reduce the IMAD.HI back into a shift.
+static __constant__ uint32_t c_pow2[32] = {
+    1u << 0,  1u << 1,  1u << 2,  1u << 3,  1u << 4,  1u << 5,  1u << 6,  1u << 7,  1u << 8,  1u << 9,  1u << 10,
+    1u << 11, 1u << 12, 1u << 13, 1u << 14, 1u << 15, 1u << 16, 1u << 17, 1u << 18, 1u << 19, 1u << 20, 1u << 21,
+    1u << 22, 1u << 23, 1u << 24, 1u << 25, 1u << 26, 1u << 27, 1u << 28, 1u << 29, 1u << 30, 1u << 31,
+};
+
+// The top LG bits of a 32-bit draw, d >> (32 - LG) (DESIGN.md section 2:
+// "bit_W(d) = d >> (32 - log2 W)").  With tuning::TOP_MULHI it is
+// IMAD.HI(d, 2^LG) on the FMA pipe instead of SHF on the ALU pipe: the draw
+// loops issue mostly ALU-pipe instructions (shifts, funnel tests, LOP3), and
+// each pipe takes one warp instruction per 2 cycles per SMSP
+// (B300_MICROARCH: fma vs alu split), so moving the extraction balances them.
+template <int LG>
+__device__ __forceinline__ uint32_t top(uint32_t d)
+{
+    static_assert(LG >= 1 && LG <= 31, "1..31 top bits");
+    if constexpr (tuning::TOP_MULHI) return __umulhi(d, c_pow2[LG]);
+    else return d >> (32 - LG);
+}
 
 // ---------------------------------------------------------------- hashing
 __device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }

@@ -40,7 +40,9 @@ void launch_probe_red(void* buf, uint64_t b, uint32_t B, uint32_t lanes, const u
 
 void launch_probe_rng(const void* buf, uint64_t b, uint32_t B, int red, uint32_t lanes, uint64_t n,
                       cudaStream_t st, int grid);
-int launch_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint64_t n,
+int launch_probe_red_pattern(void* buf, uint64_t b, uint32_t B, uint32_t S, uint32_t variant, uint32_t k, uint32_t z,
+                             uint64_t n, cudaStream_t st, int grid);
+int launch_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint32_t mlp, uint64_t n,
                       cudaStream_t st, int grid);
 
 void launch_scatter_results(const uint64_t* idx, const uint8_t* res, const unsigned long long* counts,

@@ -247,20 +247,20 @@ __device__ __forceinline__ typename C::W slot_mask(const Draws<C>& dr, uint32_t 
     if constexpr (C::V == V_SBF || C::V == V_RBBF) {
         StaticFor<0, C::Q>::run([&](auto T) {
             const uint32_t d = dr.template word_draw<SLOT, decltype(T)::value>(w, ss);
-            m |= W(1) << (d >> (32 - C::LGW));
+            m |= W(1) << top<C::LGW>(d);
         });
     } else if constexpr (C::V == V_CSBF) {
         StaticFor<0, C::Q>::run([&](auto T) {
             const uint32_t d = dr.template word_draw<SLOT, decltype(T)::value>(w, ss);
-            m |= W(1) << (d >> (32 - C::LGW));
+            m |= W(1) << top<C::LGW>(d);
         });
         if constexpr (C::G > 1) {
-            const uint32_t sel = (dr.lo * ss.template gsalt<SLOT>(w)) >> (32 - C::LGG);
+            const uint32_t sel = top<C::LGG>(dr.lo * ss.template gsalt<SLOT>(w));
             m = ((w & (C::G - 1)) == sel) ? m : W(0);
         }
     } else {  // BBF: k draws over the whole block; keep those landing in word w
         StaticFor<0, C::K>::run([&](auto J) {
-            const uint32_t p = dr.template bbf_draw<decltype(J)::value>(ss) >> (32 - C::LGB);
+            const uint32_t p = top<C::LGB>(dr.template bbf_draw<decltype(J)::value>(ss));
             m |= shl_clamp(W(1), p - w * (uint32_t)C::S);
         });
     }
@@ -276,7 +276,7 @@ __device__ __forceinline__ typename C::W group_mask(const Draws<C>& dr, uint32_t
     W m = 0;
     StaticFor<0, C::Q>::run([&](auto T) {
         const uint32_t d = dr.template word_draw<SL0, decltype(T)::value>(w0, ss);
-        m |= W(1) << (d >> (32 - C::LGW));
+        m |= W(1) << top<C::LGW>(d);
     });
     return m;
 }
@@ -318,7 +318,7 @@ __device__ __forceinline__ bool test_block(const typename C::W* wd, const Draws<
             constexpr int w = decltype(I)::value;
             StaticFor<0, C::Q>::run([&](auto T) {
                 const uint32_t d = dr.template word_draw<w, decltype(T)::value>((uint32_t)w, ss);
-                acc &= (uint32_t)(wd[w] >> (d >> (32 - C::LGW)));
+                acc &= (uint32_t)(wd[w] >> top<C::LGW>(d));
             });
         });
     } else if constexpr (C::V == V_CSBF) {
@@ -326,14 +326,14 @@ __device__ __forceinline__ bool test_block(const typename C::W* wd, const Draws<
             constexpr int w0 = decltype(I)::value * C::G;  // first word of group i
             W x;
             if constexpr (C::G > 1) {
-                const uint32_t sel = (dr.lo * ss.template gsalt<w0>((uint32_t)w0)) >> (32 - C::LGG);
+                const uint32_t sel = top<C::LGG>(dr.lo * ss.template gsalt<w0>((uint32_t)w0));
                 x = pick<C::G>(wd + w0, sel);
             } else {
                 x = wd[w0];
             }
             StaticFor<0, C::Q>::run([&](auto T) {
                 const uint32_t d = dr.template word_draw<w0, decltype(T)::value>((uint32_t)w0, ss);
-                acc &= (uint32_t)(x >> (d >> (32 - C::LGW)));
+                acc &= (uint32_t)(x >> top<C::LGW>(d));
             });
         });
     } else if constexpr (C::BBF_CLAMP) {
@@ -341,14 +341,14 @@ __device__ __forceinline__ bool test_block(const typename C::W* wd, const Draws<
         // PTX's clamping shifts (an amount >= 64, incl. a wrapped p - 64 i,
         // gives 0): no word select, no predicate
         StaticFor<0, C::K>::run([&](auto J) {
-            const uint32_t p = dr.template bbf_draw<decltype(J)::value>(ss) >> (32 - C::LGB);
+            const uint32_t p = top<C::LGB>(dr.template bbf_draw<decltype(J)::value>(ss));
             uint32_t t = shr_clamp_lo(wd[0], p);
             StaticFor<1, C::s>::run([&](auto I) { t |= shr_clamp_lo(wd[decltype(I)::value], p - 64u * decltype(I)::value); });
             acc &= t;
         });
     } else {  // BBF
         StaticFor<0, C::K>::run([&](auto J) {
-            const uint32_t p = dr.template bbf_draw<decltype(J)::value>(ss) >> (32 - C::LGB);
+            const uint32_t p = top<C::LGB>(dr.template bbf_draw<decltype(J)::value>(ss));
             const W x = (C::s > 1) ? pick<C::s>(wd, p >> C::LGW) : wd[0];
             acc &= (uint32_t)(x >> (p & (C::S - 1)));
         });
@@ -375,8 +375,8 @@ __device__ __forceinline__ bool test_block_sm(const typename C::W* wd, const Dra
     uint32_t acc = 0xffffffffu;
     StaticFor<0, C::K>::run([&](auto J) {
         const uint32_t d = dr.template bbf_draw<decltype(J)::value>(ss);
-        const uint32_t x = col[(d >> (32 - C::LGB + 5)) * 32];
-        acc &= __funnelshift_r(x, x, d >> (32 - C::LGB));
+        const uint32_t x = col[top<C::LGB - 5>(d) * 32];
+        acc &= __funnelshift_r(x, x, top<C::LGB>(d));
     });
     return acc & 1u;
 }
@@ -397,7 +397,7 @@ __device__ __forceinline__ typename C::W contains_part(const typename C::W* F, c
         StaticFor<0, C::NSLOT / C::G>::run([&](auto GI) {
             constexpr int SL0 = decltype(GI)::value * C::G;
             const W m = group_mask<C, SL0>(dr, C::word(SL0, pos), ss);
-            const uint32_t sel = (dr.lo * ss.template gsalt<SL0>(C::word(SL0, pos))) >> (32 - C::LGG);
+            const uint32_t sel = top<C::LGG>(dr.lo * ss.template gsalt<SL0>(C::word(SL0, pos)));
             acc |= m & ~pick<C::G>(wd + SL0, sel);
         });
     } else {
@@ -422,7 +422,7 @@ __device__ __forceinline__ void add_part(typename C::W* F, const Draws<C>& dr, u
             constexpr int SL0 = decltype(GI)::value * C::G;
             const uint32_t w0 = (C::THETA == 1) ? (uint32_t)SL0 : C::word(SL0, pos);
             const W m = group_mask<C, SL0>(dr, w0, ss);
-            const uint32_t sel = (dr.lo * ss.template gsalt<SL0>(w0)) >> (32 - C::LGG);
+            const uint32_t sel = top<C::LGG>(dr.lo * ss.template gsalt<SL0>(w0));
             red_or(bp + w0 + sel, m);
         });
         return;
@@ -542,8 +542,8 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
                 const Draws<C> dr(lo[j], C::HS == 1 ? lo2[j] : 0u);
                 StaticFor<0, C::K>::run([&](auto J) {
                     const uint32_t d = dr.template bbf_draw<decltype(J)::value>(ss);
-                    const uint32_t q = d >> (32 - C::LGB + 5);
-                    atomicOr(base + q * 32 + (lane ^ q), __funnelshift_l(1u, 1u, d >> (32 - C::LGB)));
+                    const uint32_t q = top<C::LGB - 5>(d);
+                    atomicOr(base + q * 32 + (lane ^ q), __funnelshift_l(1u, 1u, top<C::LGB>(d)));
                 });
             }
         }
@@ -699,7 +699,7 @@ __device__ __forceinline__ void contains_ksm(const Params& p, uint32_t* sm, uint
 }
 
 template <class C, bool ADD>
-__global__ void __launch_bounds__(256) bulk_kernel(const Params p)
+__global__ void __launch_bounds__(256, (!ADD && C::BBF_SM) ? tuning::BBF_SM_MINB : 1) bulk_kernel(const Params p)
 {
     __shared__ uint32_t s_salt[C::HV == 2 ? 64 : 1];
     __shared__ uint32_t s_gsalt[C::HV == 2 ? 16 : 1];

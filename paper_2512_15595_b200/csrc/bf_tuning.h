@@ -17,5 +17,17 @@ constexpr int L2PF_DIST = -1;
 constexpr bool BBF2_CLAMP = true;
 // Θ=1 contains stages its key stream in shared memory by cp.async (Cfg::KEY_SMEM)
 constexpr bool KEY_SMEM = true;
+// bit positions d >> (32 - lg) computed as IMAD.HI(d, 2^lg) on the FMA pipe
+// instead of a shift on the ALU pipe (top<lg>, bf_device.cuh).  Measured
+// (tools/kexp, profiles/r2_kexp.md): slower almost everywhere (SBF 256/64
+// k=16 contains 213 -> 195, BBF 128/64 k=12 add 133 -> 100 Gkeys/s): more
+// registers, fewer resident CTAs.  Off.
+constexpr bool TOP_MULHI = false;
+// minimum resident CTAs per SM requested from ptxas for the BBF contains
+// kernels that stage blocks in shared memory (Cfg::BBF_SM).  ptxas' own
+// choice for them was 64 registers with spills (48 KB of static shared
+// memory allows 4 CTAs); 3 gives 80 registers, no spills: BBF 256/64 k=12
+// 133 -> 141, k=16 119 -> 125 Gkeys/s (tools/kexp)
+constexpr int BBF_SM_MINB = 3;
 }  // namespace tuning
 }  // namespace bf

@@ -323,32 +323,96 @@ __global__ void __launch_bounds__(256) probe_gups_kernel(unsigned long long* buf
     if (!RED && acc == 0x9E3779B97F4A7C15ULL) sink[0] = acc;  // keeps the loads alive
 }
 
-int launch_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint64_t n,
-                      cudaStream_t st, int grid)
+template <int BYTES, int HINT, bool RED>
+static int gups_mlp(unsigned long long* p, uint64_t units, uint64_t n, uint32_t mlp, cudaStream_t st, int grid)
 {
-    constexpr int MLP = 8;
-    const uint64_t units = nbytes / access_bytes;
     const uint64_t threads = (uint64_t)grid * 256;
-    const uint64_t iters = (n + threads * MLP - 1) / (threads * MLP);
-    auto* p = (unsigned long long*)buf;
-#define BF_GUPS(B_, H_, R_) probe_gups_kernel<B_, H_, R_, MLP><<<grid, 256, 0, st>>>(p, units, iters, p)
-    if (red) {
-        if (access_bytes != 8) return -1;
-        BF_GUPS(8, 0, true);
-        return 0;
-    }
-    switch (access_bytes * 4 + hint) {
-    case 32: BF_GUPS(8, 0, false); break;
-    case 33: BF_GUPS(8, 1, false); break;
-    case 34: BF_GUPS(8, 2, false); break;
-    case 128: BF_GUPS(32, 0, false); break;
-    case 129: BF_GUPS(32, 1, false); break;
-    case 130: BF_GUPS(32, 2, false); break;
-    case 256: BF_GUPS(64, 0, false); break;
-    case 257: BF_GUPS(64, 1, false); break;
+    const uint64_t iters = (n + threads * mlp - 1) / (threads * mlp);
+    switch (mlp) {
+    case 1: probe_gups_kernel<BYTES, HINT, RED, 1><<<grid, 256, 0, st>>>(p, units, iters, p); break;
+    case 2: probe_gups_kernel<BYTES, HINT, RED, 2><<<grid, 256, 0, st>>>(p, units, iters, p); break;
+    case 4: probe_gups_kernel<BYTES, HINT, RED, 4><<<grid, 256, 0, st>>>(p, units, iters, p); break;
+    case 8: probe_gups_kernel<BYTES, HINT, RED, 8><<<grid, 256, 0, st>>>(p, units, iters, p); break;
+    case 16: probe_gups_kernel<BYTES, HINT, RED, 16><<<grid, 256, 0, st>>>(p, units, iters, p); break;
     default: return -1;
     }
-#undef BF_GUPS
+    return 0;
+}
+
+int launch_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint32_t mlp, uint64_t n,
+                      cudaStream_t st, int grid)
+{
+    const uint64_t units = nbytes / access_bytes;
+    auto* p = (unsigned long long*)buf;
+    if (red) return access_bytes == 8 && hint == 0 ? gups_mlp<8, 0, true>(p, units, n, mlp, st, grid) : -1;
+    switch (access_bytes * 4 + hint) {
+    case 32: return gups_mlp<8, 0, false>(p, units, n, mlp, st, grid);
+    case 33: return gups_mlp<8, 1, false>(p, units, n, mlp, st, grid);
+    case 34: return gups_mlp<8, 2, false>(p, units, n, mlp, st, grid);
+    case 128: return gups_mlp<32, 0, false>(p, units, n, mlp, st, grid);
+    case 129: return gups_mlp<32, 1, false>(p, units, n, mlp, st, grid);
+    case 130: return gups_mlp<32, 2, false>(p, units, n, mlp, st, grid);
+    case 256: return gups_mlp<64, 0, false>(p, units, n, mlp, st, grid);
+    case 257: return gups_mlp<64, 1, false>(p, units, n, mlp, st, grid);
+    default: return -1;
+    }
+}
+
+// R_red with the add's exact RED pattern but random bits (payload-matched
+// roofline of a configuration): one random block per key, a group of
+// lanes issues the REDs in one instruction as the product's add does:
+//   SBF / RBBF: s lanes, every lane ORs its word (payload B/8 per key)
+//   BBF:        s lanes, a lane ORs its word iff one of k uniform word draws
+//               hits it (payload = distinct words, s(1 - (1-1/s)^k) on
+//               average)
+//   CSBF:       z lanes, lane i ORs one uniform word of group i (payload z
+//               words)
+// Addresses and bits come from an in-register xorshift stream shared by the
+// group (no keys, no hashing).
+template <int S>
+__global__ void __launch_bounds__(256) probe_red_pattern_kernel(void* buf, uint64_t b, uint32_t s, uint32_t lgs,
+                                                                uint32_t variant, uint32_t k, uint32_t z,
+                                                                uint32_t lanes, uint64_t iters)
+{
+    using W = typename WordT<S>::T;
+    W* F = (W*)buf;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t pos = lane % lanes;
+    const uint64_t group = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32 + (lane - pos);
+    uint64_t x = mix64(group + 0x3c3cULL) | 1ULL;
+    const bool active = lane < (32 / lanes) * lanes;
+    for (uint64_t it = 0; it < iters; ++it) {
+        x = xs64(x);
+        const uint64_t blk = ((x >> 32) * b) >> 32;
+        const uint64_t y = xs64(x ^ 0x9E3779B97F4A7C15ULL);
+        uint32_t w = pos;
+        bool hit = true;
+        if (variant == V_BBF) {  // k word draws of lgs bits each from y (k * lgs <= 64)
+            hit = false;
+            for (uint32_t j = 0; j < k; ++j) hit |= ((uint32_t)(y >> (j * lgs)) & (s - 1)) == pos;
+        } else if (variant == V_CSBF) {
+            const uint32_t g = s / z;
+            w = pos * g + ((uint32_t)(y >> ((pos * 5) % 60)) & (g - 1));
+        }
+        if (active && hit) red_or(F + blk * s + w, W(1) << ((uint32_t)(x >> (8 * (pos & 3))) & (S - 1)));
+    }
+}
+
+int launch_probe_red_pattern(void* buf, uint64_t b, uint32_t B, uint32_t S, uint32_t variant, uint32_t k, uint32_t z,
+                             uint64_t n, cudaStream_t st, int grid)
+{
+    const uint32_t s = B / S;
+    uint32_t lgs = 0;
+    while ((1u << lgs) < s) ++lgs;
+    const uint32_t lanes = variant == V_CSBF ? z : s;
+    if (!lanes || lanes > 32 || (variant == V_BBF && k * lgs > 64) || (variant == V_CSBF && (s % z || (s / z) > 32)))
+        return -1;
+    const uint64_t groups = (uint64_t)grid * 256 / 32 * (32 / lanes);
+    const uint64_t iters = (n + groups - 1) / groups;
+    if (S == 64)
+        probe_red_pattern_kernel<64><<<grid, 256, 0, st>>>(buf, b, s, lgs, variant, k, z, lanes, iters);
+    else
+        probe_red_pattern_kernel<32><<<grid, 256, 0, st>>>(buf, b, s, lgs, variant, k, z, lanes, iters);
     return 0;
 }
 

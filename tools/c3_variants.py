@@ -1,0 +1,146 @@
+"""configs[2] (BASELINE.json): register-blocked vs sectorized
+vs cache-sectorized vs blocked filters on an 8 GiB HBM-resident filter with
+2^32 keys, one B200.
+
+Per variant (RBBF 64/64 k=6, SBF 256/64 k=8, CSBF 256/32 z=4 k=8, CSBF 256/32
+z=2 k=8, BBF 256/64 k=8): add of all 2^32 keys (the library default: binned;
+and the direct add for comparison), contains of all 2^32 positives, contains
+of 2^28 negatives (FPR against the exact model, profiles/iso_fpr_table.json
+"c3", written from oracle/ only), and parity on a sampled block range (the
+range-restricted oracle hashes all 2^32 keys, generated on the host from the
+same indices, and stores only that range).
+
+Usage (GPU box): python tools/c3_variants.py OUT_PREFIX   -> OUT_PREFIX.jsonl / .md
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+import statistics
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+from oracle.bfo import OracleFilter  # noqa: E402
+from paper_2512_15595_b200 import bf  # noqa: E402
+
+NAMES = {1: "BBF", 2: "RBBF", 3: "SBF", 4: "CSBF"}
+
+
+def timed(fn, reps=3):
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0.record(st)
+        fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+def oracle_ranges(specs, n, chunk=1 << 25):
+    """Bytes of block ranges [lo, hi) of the filters built from all n keys
+    (range-restricted oracle: every key is hashed, only the range is stored)."""
+    accs = [np.zeros((hi - lo) * geo.B // 8, dtype=np.uint8) for geo, lo, hi in specs]
+    th = os.cpu_count() or 4
+    offs = list(range(0, n, chunk))
+    with ThreadPoolExecutor(2) as ex:
+        fut = ex.submit(synth.keys, 0, min(chunk, n))
+        for i, off in enumerate(offs):
+            kc = fut.result()
+            if i + 1 < len(offs):
+                nxt = offs[i + 1]
+                fut = ex.submit(synth.keys, nxt, min(chunk, n - nxt))
+            for (geo, lo, hi), acc in zip(specs, accs):
+                acc |= geo.add_range(kc, lo, hi, threads=th)
+    return accs
+
+
+def main():
+    out_prefix = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/c3_variants"
+    tab = json.load(open(os.path.join(ROOT, "profiles", "iso_fpr_table.json")))["c3"]
+    m, n, q = tab["m_bits"], tab["n"], 1 << 28
+    dev = torch.device("cuda:0")
+    keys = torch.empty(n, dtype=torch.int64, device=dev)
+    bf.bf_keygen(keys, n, 0)
+    neg = torch.empty(q, dtype=torch.int64, device=dev)
+    bf.bf_keygen(neg, q, synth.NEG_BASE)
+    out = torch.empty(n // 32, dtype=torch.int32, device=dev)
+    outn = torch.empty(q // 32, dtype=torch.int32, device=dev)
+    lut = torch.tensor([bin(i).count("1") for i in range(256)], dtype=torch.int32, device=dev)
+    rows, checks = [], []
+    for row in tab["rows"]:
+        v, B, S, k, z = row["variant"], row["B"], row["S"], row["k"], row["z"]
+        f = bf.Filter(m, k, B, S, v, z=z)
+
+        def add():
+            f.clear()
+            f.add(keys)
+        t_add = timed(add)
+        binned = f.add_mode()[1]
+        f.set_add_mode(bf.BF_ADD_DIRECT)
+        t_direct = timed(add, 1)
+        f.set_add_mode(bf.BF_ADD_AUTO)
+        add()
+        t_con = timed(lambda: f.contains(keys, out))
+        fn_ok = int((out != -1).sum().item()) == 0
+        t_neg = timed(lambda: f.contains(neg, outn))
+        fp = int(lut[outn.view(torch.uint8).long()].sum().item())
+        p = row["fpr_model"]
+        zz = (fp - q * p) / math.sqrt(q * p * (1 - p))
+        # parity on a sampled range (middle of the filter, 2^14 blocks), checked after the loop
+        geo = OracleFilter(v, m, B=B, S=S, k=k, z=z, allocate=False)
+        lo = geo.b // 2 - 7777
+        hi = lo + (1 << 14)
+        got = f.data()[lo * B // 8: hi * B // 8].cpu().numpy()
+        checks.append((geo, lo, hi, got))
+        par = None
+        rec = {"config": "configs[2]", "variant": NAMES[v], "B": B, "S": S, "k": k, "z": z, "m_bits": m, "n": n,
+               "add_gkeys_s": round(n / t_add / 1e6, 3), "add_path": "binned" if binned else "direct",
+               "add_direct_gkeys_s": round(n / t_direct / 1e6, 3),
+               "contains_gkeys_s": round(n / t_con / 1e6, 3), "contains_neg_gkeys_s": round(q / t_neg / 1e6, 3),
+               "step_gkeys_s": round(2 * n / (t_add + t_con) / 1e6, 3),
+               "fpr_measured": fp / q, "fpr_model": p, "fpr_z": round(zz, 2), "negatives": q,
+               "no_false_negatives": fn_ok, "parity_sampled_range": [lo, hi], "parity": par,
+               "layout_add": f.layout(0), "layout_contains": f.layout(1)}
+        print(json.dumps(rec), flush=True)
+        rows.append(rec)
+        del f
+        torch.cuda.empty_cache()
+    del keys, neg, out, outn
+    # one pass over the host-generated keys for every variant's sampled range
+    wants = oracle_ranges([(g, lo, hi) for g, lo, hi, _ in checks], n)
+    for r, (g, lo, hi, got), want in zip(rows, checks, wants):
+        r["parity"] = "bit-exact" if np.array_equal(got, want) else "FAIL"
+        print(json.dumps({"variant": r["variant"], "z": r["z"], "parity": r["parity"]}), flush=True)
+    with open(out_prefix + ".jsonl", "w") as fh:
+        for r in rows:
+            fh.write(json.dumps(r) + "\n")
+    with open(out_prefix + ".md", "w") as fh:
+        fh.write("# configs[2]: five filter variants at 8 GiB (HBM-resident), 2^32 keys, one B200\n\n"
+                 "`tools/c3_variants.py`. Gkeys/s, CUDA-event median. add = library default (binned), "
+                 "direct = bf_add with BF_ADD_DIRECT. FPR on 2^28 negatives vs the exact model; parity: "
+                 "a 2^14-block range in the middle of the filter equals the range-restricted oracle's "
+                 "(all 2^32 keys hashed on the host).\n\n")
+        fh.write("| variant | B/S | k | z | add (binned) | add (direct) | contains pos | contains neg | "
+                 "add+contains | FPR measured | FPR model | z | FN | parity |\n"
+                 "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
+        for r in rows:
+            fh.write(f"| {r['variant']} | {r['B']}/{r['S']} | {r['k']} | {r['z']} | {r['add_gkeys_s']} | "
+                     f"{r['add_direct_gkeys_s']} | {r['contains_gkeys_s']} | {r['contains_neg_gkeys_s']} | "
+                     f"{r['step_gkeys_s']} | {r['fpr_measured']:.3e} | {r['fpr_model']:.3e} | {r['fpr_z']:+.1f} | "
+                     f"{'none' if r['no_false_negatives'] else 'FOUND'} | {r['parity']} |\n")
+
+
+if __name__ == "__main__":
+    main()

@@ -47,6 +47,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--grans", default="0,32,64,128")
     ap.add_argument("--no-product", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="MLP x CTAs sweep at the default granularity")
+    ap.add_argument("--sweep2", action="store_true", help="fine CTA sweep at MLP 1/2, product KPT/CTA variants")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
@@ -62,6 +64,62 @@ def main():
         f.set_add_mode(bf.BF_ADD_DIRECT)
         f.add(keys)
     base = bf.bf_get_l2_fetch_granularity()
+    if a.sweep2:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        for rep in range(2):
+            for mlp in (1, 2):
+                for cps in (8, 9, 10, 11, 12, 14, 16, 20, 24, 32):
+                    ms = timed(lambda: bf.bf_probe_gups(buf, nbytes, 32, 0, 1, n, mlp, cps * sms), 9)
+                    print(json.dumps({"probe": "gups_read_32_L2_64B", "rep": rep, "mlp": mlp, "ctas_per_sm": cps,
+                                      "n": n, "ms": round(ms, 4), "g_per_s": round(n / (ms * 1e-3) / 1e9, 3)}), flush=True)
+            ms = timed(lambda: bf.bf_probe_read(buf, nbytes // 32, 256, keys, out), 9)
+            print(json.dumps({"probe": "block_read_keys_B256", "rep": rep, "n": n, "ms": round(ms, 4),
+                              "g_per_s": round(n / (ms * 1e-3) / 1e9, 3)}), flush=True)
+        if f is not None:
+            for kpt in (4,):
+                f.set_layout(1, 1, 4, kpt, 0)
+                occ = bf.bf_get_launch(f.handle, 1)[1]
+                for cps in sorted({1, 2, occ, 4, 6, 8, 10, 12, 16, 24, 32}):
+                    f.set_launch(1, cps)
+                    ms = timed(lambda: f.contains(keys, out), 9)
+                    print(json.dumps({"probe": "product_contains_sbf256_k8", "kpt": kpt, "ctas_per_sm": cps,
+                                      "occupancy": occ, "n": n, "ms": round(ms, 4),
+                                      "g_per_s": round(n / (ms * 1e-3) / 1e9, 3)}), flush=True)
+                f.set_launch(1, 0)
+            occ = bf.bf_get_launch(f.handle, 0)[1]
+            for cps in sorted({1, 2, occ, 8, 10, 12, 16, 24, 32}):
+                f.set_launch(0, cps)
+                ms = timed(lambda: f.add(keys), 5)
+                print(json.dumps({"probe": "product_add_direct_sbf256_k8", "ctas_per_sm": cps, "occupancy": occ,
+                                  "n": n, "ms": round(ms, 4), "g_per_s": round(n / (ms * 1e-3) / 1e9, 3)}), flush=True)
+            f.set_launch(0, 0)
+        for mlp in (1, 8):  # updates, fine CTA sweep
+            for cps in (8, 10, 12, 16, 24):
+                ms = timed(lambda: bf.bf_probe_gups(buf, nbytes, 8, 1, 0, n, mlp, cps * sms), 5)
+                print(json.dumps({"probe": "gups_update_8", "mlp": mlp, "ctas_per_sm": cps, "n": n, "ms": round(ms, 4),
+                                  "g_per_s": round(n / (ms * 1e-3) / 1e9, 3)}), flush=True)
+        return
+    if a.sweep:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        for name, ab, red, hint in (("gups_read_8", 8, 0, 0), ("gups_read_32_L2_64B", 32, 0, 1),
+                                    ("gups_update_8", 8, 1, 0)):
+            for mlp in (1, 2, 4, 8, 16):
+                for cps in (1, 2, 4, 8):
+                    ms = timed(lambda: bf.bf_probe_gups(buf, nbytes, ab, red, hint, n, mlp, cps * sms), a.reps)
+                    print(json.dumps({"probe": name, "mlp": mlp, "ctas_per_sm": cps, "threads_in_flight": cps * sms * 256,
+                                      "accesses_in_flight": cps * sms * 256 * mlp, "buffer_gib": a.gib, "n": n,
+                                      "ms": round(ms, 4), "g_per_s": round(n / (ms * 1e-3) / 1e9, 3)}), flush=True)
+        if f is not None:
+            occ = [bf.bf_get_launch(f.handle, op)[1] for op in (0, 1)]
+            for op, name, fn in ((1, "product_contains_sbf256_k8", lambda: f.contains(keys, out)),
+                                 (0, "product_add_direct_sbf256_k8", lambda: f.add(keys))):
+                for cps in range(1, occ[op] + 1):
+                    f.set_launch(op, cps)
+                    ms = timed(fn, a.reps)
+                    print(json.dumps({"probe": name, "ctas_per_sm": cps, "occupancy": occ[op], "n": n,
+                                      "ms": round(ms, 4), "g_per_s": round(n / (ms * 1e-3) / 1e9, 3)}), flush=True)
+                f.set_launch(op, 0)
+        return
     probes = [
         ("gups_read_8", lambda: bf.bf_probe_gups(buf, nbytes, 8, 0, 0, n)),
         ("gups_read_8_L2_64B", lambda: bf.bf_probe_gups(buf, nbytes, 8, 0, 1, n)),

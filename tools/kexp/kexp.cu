@@ -79,19 +79,21 @@ static void run(Ctx& c, const char* name)
     // add timing (each rep re-adds the same keys: idempotent)
     CK(cudaMemset(c.words, 0, c.m_bits / 8));
     p.keys = c.keys;
-    float ta = time_kernel(c, bulk_kernel<CA, true>, p, occA * nsm, true);
+    const char* ov = getenv("KEXP_CPS");  // CTAs per SM (waves) instead of the occupancy grid
+    const int gA = ov ? atoi(ov) * nsm : occA * nsm, gC = ov ? atoi(ov) * nsm : occC * nsm;
+    float ta = time_kernel(c, bulk_kernel<CA, true>, p, gA, true);
     std::vector<unsigned char> fb(c.m_bits / 8);
     CK(cudaMemcpy(fb.data(), c.words, fb.size(), cudaMemcpyDeviceToHost));
     // contains on the positives
     p.out = c.out;
-    float tc = time_kernel(c, bulk_kernel<CC, false>, p, occC * nsm);
+    float tc = time_kernel(c, bulk_kernel<CC, false>, p, gC);
     std::vector<uint32_t> ob((c.n + 31) / 32);
     CK(cudaMemcpy(ob.data(), c.out, ob.size() * 4, cudaMemcpyDeviceToHost));
     uint64_t pc = 0;
     for (uint32_t w : ob) pc += __builtin_popcount(w);
     // negatives (false positives)
     p.keys = c.neg;
-    float tn = time_kernel(c, bulk_kernel<CC, false>, p, occC * nsm);
+    float tn = time_kernel(c, bulk_kernel<CC, false>, p, gC);
     CK(cudaMemcpy(ob.data(), c.out, ob.size() * 4, cudaMemcpyDeviceToHost));
     uint64_t fp = 0;
     for (uint32_t w : ob) fp += __builtin_popcount(w);
@@ -207,7 +209,7 @@ static void run_binned(Ctx& c, const char* name, uint32_t range_kb, const char* 
     bp.cap = cap;
     bp.lg_bpr = lg;
     bp.nranges = R;
-    const size_t sm_bin = bin_smem_bytes(R, NT * BK);
+    const size_t sm_bin = bin_smem_bytes(R, false, NT * BK);
     CK(cudaFuncSetAttribute(bin_kernel<C1, NT, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bin));
     const size_t sm_app = (size_t)(1u << lg) * (B / 8);
     CK(cudaFuncSetAttribute(apply_smem_kernel<C1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_app));
@@ -281,13 +283,15 @@ static void run_bin(Ctx& c, const char* name, uint32_t range_kb)
     bp.lg_bpr = lg;
     bp.nranges = R;
     auto kern = bin_kernel<C1, NT, BK>;
-    const size_t sm = bin_smem_bytes(R, NT * BK);
+    const size_t sm = bin_smem_bytes(R, false, NT * BK);
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int nsm = 0, occ = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, sm));
     const uint64_t chunks = (c.n + NT * BK - 1) / (NT * BK);
-    const int gb = (int)std::min<uint64_t>(chunks, (uint64_t)occ * nsm);
+    const char* ov = getenv("KEXP_BIN_CPS");  // CTAs per SM (waves) instead of the occupancy grid
+    const int cps = ov ? atoi(ov) : occ;
+    const int gb = (int)std::min<uint64_t>(chunks, (uint64_t)cps * nsm);
     std::vector<float> ts;
     uint64_t sum = 0;
     for (int r = 0; r < c.reps + 2; ++r) {
@@ -312,9 +316,9 @@ static void run_bin(Ctx& c, const char* name, uint32_t range_kb)
         for (uint64_t i = 0; i < std::min<uint64_t>(cur[r], cap); ++i) x ^= hr[r * cap + i] * 0x9E3779B97F4A7C15ULL + r;
     }
     std::sort(ts.begin(), ts.end());
-    printf("{\"cfg\": \"%s\", \"bin\": \"%s\", \"nt\": %d, \"bk\": %d, \"R\": %u, \"occ\": %d, \"bin_ms\": %.4f, "
+    printf("{\"cfg\": \"%s\", \"bin\": \"%s\", \"nt\": %d, \"bk\": %d, \"R\": %u, \"occ\": %d, \"grid\": %d, \"bin_ms\": %.4f, "
            "\"gkeys_s\": %.2f, \"total\": %llu, \"xor\": \"%016llx\"}\n",
-           name, REG ? "reg" : "staged", NT, BK, R, occ, ts[ts.size() / 2], c.n / ts[ts.size() / 2] / 1e6,
+           name, REG ? "reg" : "staged", NT, BK, R, occ, gb, ts[ts.size() / 2], c.n / ts[ts.size() / 2] / 1e6,
            (unsigned long long)tot, (unsigned long long)x);
     fflush(stdout);
     (void)sum;
@@ -428,6 +432,19 @@ int main(int argc, char** argv)
             run_bin<SBF8, 256, 4, false>(c, "SBF256/64 k8", kb);
             run_bin<SBF8, 128, 8, false>(c, "SBF256/64 k8", kb);
             run_bin<SBF8, 512, 4, false>(c, "SBF256/64 k8", kb);
+        }
+        return 0;
+    }
+    if (argc > 1 && strcmp(argv[1], "bin2") == 0) {  // bin phase only: R = 256 buckets (128 KB ranges)
+        using SBF8 = Cfg<V_SBF, 64, 2, 8, 0, 1, 4, 1, 0>;
+        for (int rep = 0; rep < 1; ++rep) {
+            run_bin<SBF8, 256, 16, false>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 256, 8, false>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 512, 8, false>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 128, 16, false>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 256, 12, false>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 512, 16, false>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 1024, 8, false>(c, "SBF256/64 k8", 128);
         }
         return 0;
     }

@@ -14,11 +14,19 @@
 #ifndef BF_KEY_SMEM
 #define BF_KEY_SMEM 1
 #endif
+#ifndef BF_TOP_MULHI
+#define BF_TOP_MULHI 0
+#endif
+#ifndef BF_BBF_SM_MINB
+#define BF_BBF_SM_MINB 3
+#endif
 namespace bf {
 namespace tuning {
 constexpr int T1_PF_MODE = BF_T1_PF_MODE;
 constexpr int L2PF_DIST = BF_L2PF_DIST;
 constexpr bool BBF2_CLAMP = BF_BBF2_CLAMP;
 constexpr bool KEY_SMEM = BF_KEY_SMEM;
+constexpr bool TOP_MULHI = BF_TOP_MULHI;
+constexpr int BBF_SM_MINB = BF_BBF_SM_MINB;
 }  // namespace tuning
 }  // namespace bf

@@ -42,7 +42,36 @@ def n_iso(v, B, S, k, z, m_bits, target):
     return lo
 
 
+# the sweep's 3 extra rows (gen_instances.C2_EXTRA): one-word BBF, BBF with 32-bit words
+EXTRA = [(BBF, 64, 64, 8, 0), (BBF, 256, 32, 8, 0), (BBF, 256, 32, 11, 0)]
+# configs[2]: the five variants compared at 8 GiB / 2^32 keys
+C3 = [(RBBF, 64, 64, 6, 0), (SBF, 256, 64, 8, 0), (CSBF, 256, 32, 8, 4), (CSBF, 256, 32, 8, 2), (BBF, 256, 64, 8, 0)]
+
+
 def main():
+    path = os.path.join(ROOT, "profiles", "iso_fpr_table.json")
+    if "--add-missing" in sys.argv and os.path.exists(path):
+        out = json.load(open(path))
+        have = {(r["variant"], r["B"], r["S"], r["k"], r["z"]) for r in out["c2"]["rows"]}
+        m = out["c2"]["m_bits"]
+        for v, B, S, k, z in EXTRA:
+            if (v, B, S, k, z) in have:
+                continue
+            n = n_iso(v, B, S, k, z, m, 1e-3)
+            out["c2"]["rows"].append({"variant": v, "B": B, "S": S, "k": k, "z": z, "n_iso": n,
+                                      "c_iso": m / n, "fpr_model": M.fpr_exact(v, n, m // B, B, S, k, z),
+                                      "fill_model": M.fill_exact(v, n, m // B, B, S, k, z)})
+            print("extra", v, B, S, k, z, n, flush=True)
+        m3, n3 = 1 << 36, 1 << 32
+        out["c3"] = {"m_bits": m3, "n": n3, "rows": []}
+        for v, B, S, k, z in C3:
+            f = M.fpr_exact(v, n3, m3 // B, B, S, k, z)
+            out["c3"]["rows"].append({"variant": v, "B": B, "S": S, "k": k, "z": z, "fpr_model": f,
+                                      "fill_model": M.fill_exact(v, n3, m3 // B, B, S, k, z)})
+            print("c3", v, B, S, k, z, f, flush=True)
+        json.dump(out, open(path, "w"), indent=1)
+        print("wrote", path)
+        return
     out = {"_source": "tools/make_iso_table.py (oracle/fpr_model.py exact ideal-hash model)",
            "c2": {"m_bits": 1 << 28, "target_fpr": 1e-3, "rows": []}}
     m = 1 << 28

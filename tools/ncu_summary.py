@@ -67,6 +67,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "inst": 1, "reques
 
 
 def full(path, n_keys=None):
+    """n_keys: one count, or "ADD:CONTAINS" (per-key rows use the launch's own count)."""
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, units = rows[0], rows[1]
@@ -81,14 +82,16 @@ def full(path, n_keys=None):
                 i = h.index(key)
                 print(f"| {label} (`{key}`) | {r[i]} {units[i]} |")
         if n_keys:
+            na, _, nc = str(n_keys).partition(":")
+            nk = float(na) if name.rstrip().endswith(", 1>(Params)") else float(nc or na)
             for key, label, mul in PER_KEY:
                 if key in h:
                     i = h.index(key)
                     try:
-                        v = float(r[i].replace(",", "")) * SCALE.get(units[i], 1) * mul / float(n_keys)
+                        v = float(r[i].replace(",", "")) * SCALE.get(units[i], 1) * mul / nk
                     except ValueError:
                         continue
-                    print(f"| {label} (n = {int(n_keys)}) | {v:.3f} |")
+                    print(f"| {label} (n = {int(nk)}) | {v:.3f} |")
         items = []
         for i, c in enumerate(h):
             if c.startswith("smsp__pcsamp_warps_issue_stalled_") and not c.endswith("_not_issued"):
@@ -119,9 +122,14 @@ def traffic(path, n_keys, out_json):
         acc[r[h.index("Kernel Name")]].append(b)
     old = json.load(open(out_json)) if os.path.exists(out_json) else {"kernels": {}}
     old["source"] = "ncu --set full captures (dram__bytes_read.sum + dram__bytes_write.sum per launch), one entry per kernel and key count"
+    # n_keys: one count for every kernel, or "ADD:CONTAINS" (bulk_kernel<..., 1> is add)
+    na, _, nc = str(n_keys).partition(":")
+    nc = nc or na
     for k, v in acc.items():
-        old["kernels"][f"{k} [n={int(n_keys)}]"] = {"dram_bytes_per_launch": sum(v) / len(v), "n": int(n_keys),
-                                                    "capture": os.path.basename(path)}
+        n = int(na) if k.rstrip().endswith(", 1>(Params)") else int(nc)
+        old["kernels"][f"{k} [n={n}]"] = {"dram_bytes_per_launch": sum(v) / len(v), "n": n,
+                                          "dram_bytes_per_key": sum(v) / len(v) / n,
+                                          "capture": os.path.basename(path)}
     json.dump(old, open(out_json, "w"), indent=1)
 
 

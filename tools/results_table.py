@@ -49,18 +49,22 @@ def parity_from_junit(path):
 
 
 def main(sweep, iso, junit, out):
-    rows = {}
+    rows, live = {}, {}
     for l in open(sweep):
         d = json.loads(l)
         key = (d["variant"], d["B"], d["S"], d["k"], d["z"])
+        if d["op"] == "probe":  # live per-row probes (tools/sweep.py row_probes)
+            live[key] = d
+            continue
         r = rows.setdefault(key, {"add": [], "contains": []})
-        r[d["op"]].append(d)
+        if d["op"] in r:
+            r[d["op"]].append(d)
     isod = {}
     for l in open(iso):
         d = json.loads(l)
         isod[(d["variant"], d["B"], d["S"], d["k"], d["z"])] = d
     par = parity_from_junit(junit)
-    read, red = probes(os.path.join(ROOT, "profiles", "r1_probe_red_payload.jsonl"))
+    read, red = probes(os.path.join(ROOT, "profiles", "r1_probe_red_payload.jsonl"))  # fallback only
     out_rows = []
     for key in sorted(rows):
         v, B, S, k, z = key
@@ -73,15 +77,19 @@ def main(sweep, iso, junit, out):
                 "contains": next((d for d in r["contains"]
                                   if (d["theta"], d["phi"], d["kpt"], d["hv"]) == (tc, s // tc, 4, 0)), None)}
         # probe denominators (summarize_sweep.py): contains R_read(B); add R_red(payload)
-        pr_a, pl = red_bound(red, payload(v, B, S, k, z))
-        pr_c = read.get(max(B, 64))
+        if key in live:  # payload-matched R_red (the add's own RED pattern) and R_read(B), same run
+            pr_a, pl = live[key]["red"], "pattern"
+            pr_c = live[key]["read"]
+        else:
+            pr_a, pl = red_bound(red, payload(v, B, S, k, z))
+            pr_c = read.get(max(B, 64))
         i = isod.get(key, {})
         row = {"config": "configs[1]", "variant": NAMES[v], "B": B, "S": S, "k": k, "z": z,
                "m_bits": 1 << 28, "residency": "L2", "n_keys": best["add"]["n"] if "add" in best else None,
                "add_gkeys_s": best["add"]["gkeys_s"], "add_sched": [best["add"][x] for x in ("theta", "phi", "kpt", "hv")],
                "add_default_gkeys_s": dflt["add"]["gkeys_s"] if dflt["add"] else None,
                "add_probe_gkeys_s": pr_a, "add_pct_roofline": round(100 * best["add"]["gkeys_s"] / pr_a, 1),
-               "add_probe": f"R_red({pl} B payload)",
+               "add_probe": "R_red(the add's RED pattern, live)" if pl == "pattern" else f"R_red({pl} B payload)",
                "contains_gkeys_s": best["contains"]["gkeys_s"],
                "contains_sched": [best["contains"][x] for x in ("theta", "phi", "kpt", "hv")],
                "contains_default_gkeys_s": dflt["contains"]["gkeys_s"] if dflt["contains"] else None,

@@ -51,6 +51,7 @@ def main():
     ap.add_argument("--cfg", default=None, help="v,B,S,k,z for --set one")
     ap.add_argument("--out", default=None)
     ap.add_argument("--only-variant", type=int, default=None, help="restrict c2 to one variant id")
+    ap.add_argument("--no-probe", action="store_true", help="c2: skip the per-row probes")
     a = ap.parse_args()
 
     import torch
@@ -98,6 +99,9 @@ def main():
         v, B, S, k, z = cfg
         m = m_of(cfg)
         f = bf.Filter(m, k, B, S, v, z=z)
+        # like-for-like Θ sweep: the direct add for every schedule (the
+        # binned add is one separate row below, default schedule)
+        f.set_add_mode(bf.BF_ADD_DIRECT)
         for op, th, ph, kpt, hv in sorted(scheds):
             f.set_layout(op, th, ph, kpt, hv)
             ts = []
@@ -120,9 +124,34 @@ def main():
             print(json.dumps(rec), flush=True)
             if fh:
                 fh.write(json.dumps(rec) + "\n")
+        if a.set == "c2" and not a.no_probe:  # live, geometry- and payload-matched probes of this row
+            rec = row_probes(bf, torch, dev, cfg, m, keys, out, a.reps)
+            print(json.dumps(rec), flush=True)
+            if fh:
+                fh.write(json.dumps(rec) + "\n")
         # restore default and check all-true after the sweep (sanity)
         f.set_layout(0, 0, 0)
         f.set_layout(1, 0, 0)
+        if m // 8 >= (96 << 20):  # HBM-resident: the binned add, default schedule, as its own row
+            f.set_add_mode(bf.BF_ADD_BINNED)
+            ts = []
+            for r in range(a.reps + 1):
+                f.clear()
+                e0.record(st)
+                f.add(keys)
+                e1.record(st)
+                torch.cuda.synchronize()
+                if r:
+                    ts.append(e0.elapsed_time(e1))
+            t = statistics.median(ts)
+            lay = f.layout(0)
+            rec = {"set": a.set, "variant": v, "B": B, "S": S, "k": k, "z": z, "m_bits": m, "n": n,
+                   "op": "add_binned", "theta": lay["theta"], "phi": lay["phi"], "kpt": lay["kpt"], "hv": 0,
+                   "ms": round(t, 4), "gkeys_s": round(n / (t * 1e-3) / 1e9, 3)}
+            print(json.dumps(rec), flush=True)
+            if fh:
+                fh.write(json.dumps(rec) + "\n")
+            f.set_add_mode(bf.BF_ADD_DIRECT)
         f.clear()
         f.add(keys)
         f.contains(keys, out)
@@ -130,6 +159,54 @@ def main():
         if n % 32 == 0:
             assert int((out != -1).sum()) == 0, f"false negatives in {cfg}"
         del f
+
+
+def row_probes(bf, torch, dev, cfg, m, keys, out, reps):
+    """The row's roofline denominators, measured live on a buffer of the
+    filter's size in two launch shapes (8 and 32 CTAs per SM):
+    contains -- R_read(B): one random block load per key (key-stream and
+    in-register forms); add -- R_red with the add's own RED pattern
+    (bf_probe_red_pattern: s words for SBF/RBBF, the distinct words of k
+    draws for BBF, z words for CSBF, one group instruction per key)."""
+    v, B, S, k, z = cfg
+    nbytes = m // 8
+    buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    Bp = max(64, B)
+    b = nbytes * 8 // Bp
+    bb = nbytes * 8 // B
+    n = keys.numel()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+
+    def best(fn):
+        fn()
+        ts = []
+        for _ in range(reps):
+            e0.record(st)
+            fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return min(ts)
+
+    res = {}
+    for cps in (8, 32):
+        bf.bf_set_probe_launch(cps)
+        thr = sms * cps * 256
+        n_rng = -(-n // (thr * 4)) * thr * 4
+        lanes = z if v == 4 else B // S
+        groups = thr // 32 * (32 // lanes)
+        n_pat = -(-n // groups) * groups
+        res[f"read_keys@{cps}"] = n / best(lambda: bf.bf_probe_read(buf, b, Bp, keys, out)) / 1e6
+        res[f"read_rng@{cps}"] = n_rng / best(lambda: bf.bf_probe_rng(buf, b, Bp, 0, 1, n)) / 1e6
+        res[f"red_pattern@{cps}"] = n_pat / best(lambda: bf.bf_probe_red_pattern(buf, bb, B, S, v, k, z, n)) / 1e6
+    bf.bf_set_probe_launch(0)
+    del buf
+    res = {kk: round(vv, 3) for kk, vv in res.items()}
+    return {"set": "c2", "variant": v, "B": B, "S": S, "k": k, "z": z, "m_bits": m, "n": n, "op": "probe",
+            "read": max(vv for kk, vv in res.items() if kk.startswith("read")),
+            "red": max(vv for kk, vv in res.items() if kk.startswith("red")), "forms": res}
 
 
 # the paper's Table 1 (1 GB, P:L314-338) and Table 2 (32 MB, P:L359-383), G keys/s
