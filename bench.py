@@ -518,10 +518,11 @@ def run_probes_l2(bf, torch, cfg, dev, n=1 << 26):
     (the asymptotic rate: no launch ramp or tail) and in two launch shapes
     (8 CTAs/SM persistent-style and 32 CTAs/SM waves, the product's shape):
     the key-stream forms (same key loads as the product, no hashing), the
-    in-register address forms, and for add the LSU+TMA form (half the warps
-    OR whole blocks with cp.reduce.async.bulk, half issue RED.64s).  The
-    denominator is the best of the forms and shapes for the same access
-    pattern."""
+    in-register address forms, for add the configuration's own RED pattern
+    (precomputed block + word-hit records: the add's memory traffic without
+    hashing) and the LSU+TMA form (half the warps OR whole blocks with
+    cp.reduce.async.bulk, half issue RED.64s).  The denominator is the best
+    of the forms and shapes (the strictest)."""
     B = max(64, cfg["B"])
     nbytes = cfg["m_bits"] // 8
     buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
@@ -531,11 +532,15 @@ def run_probes_l2(bf, torch, cfg, dev, n=1 << 26):
     b = nbytes * 8 // B
     lanes = max(1, B // 64)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    recs = torch.empty(n, dtype=torch.int64, device=dev)  # the add's own RED pattern (word-hit records)
+    bf.bf_probe_pattern_records(recs, n, nbytes * 8 // cfg["B"], cfg["B"], cfg["S"], VARIANT_IDS[cfg["variant"]],
+                                cfg["k"], cfg["z"], 1)
     res = {}
     for cps in (8, 32):
         bf.bf_set_probe_launch(cps)
         thr = sms * cps * 256
         forms = {"read_keys": (lambda: bf.bf_probe_read(buf, b, B, keys, out), n),
+                 "red_pattern": (lambda: bf.bf_probe_red_records(buf, cfg["B"], cfg["S"], recs, n), n),
                  "read_rng": (lambda: bf.bf_probe_rng(buf, b, B, 0, 1, n), _rng_accesses(n, thr * 4)),
                  "red_keys": (lambda: bf.bf_probe_red(buf, b, B, lanes, keys), n),
                  "red_rng": (lambda: bf.bf_probe_rng(buf, b, B, 1, lanes, n), _rng_accesses(n, thr // lanes))}
@@ -552,7 +557,7 @@ def run_probes_l2(bf, torch, cfg, dev, n=1 << 26):
                         + " / ".join(f"{k} {v}" for k, v in read.items()) + " Gkeys/s (form@CTAs per SM)")
     res["red_name"] = (f"R_red^L2(B={B}): {lanes} lanes x RED.64 into one block per key, no hash, 2^26 keys; best of "
                        + " / ".join(f"{k} {v}" for k, v in red.items()) + " Gkeys/s (form@CTAs per SM)")
-    del buf, keys, out
+    del buf, keys, out, recs
     torch.cuda.empty_cache()
     return res
 

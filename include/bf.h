@@ -273,15 +273,21 @@ int bf_probe_rng(void* buf, uint64_t b, uint32_t block_bits, int red, uint32_t l
 
 /* R_red with the add's exact RED pattern (payload-matched roofline of a
  * configuration; SURVEY 8(d) "% of roofline = our Gkeys/s / the probe with
- * the same (B, S, Θ, atomics per key) geometry"): n keys, each one random
- * block of a b-block buffer, the REDs of a key issued by one group of lanes
- * in one instruction as bf_add's default schedule does -- SBF/RBBF: all s
- * words; BBF: the distinct words hit by k uniform word draws; CSBF (z): one
- * uniform word of each of the z groups.  Bits are random (no keys, no
- * hashing).  The arguments must form a valid configuration (bf_create's
- * rules; BF_EINVAL otherwise). */
-int bf_probe_red_pattern(void* buf, uint64_t b, uint32_t block_bits, uint32_t word_bits, uint32_t variant,
-                         uint32_t k, uint32_t z, uint64_t n, void* stream);
+ * the same (B, S, Θ, atomics per key) geometry").
+ *   bf_probe_pattern_records (setup, untimed): recs[i] = (block << 32) |
+ *     word-hit mask for n synthetic keys: block uniform in [0, b), and the
+ *     words the configuration's pattern touches for a uniform lo (SBF/RBBF:
+ *     all s words; BBF: the words of its k draws; CSBF: one word per group),
+ *     by the rules of DESIGN.md section 2.  A valid configuration (bf_create's
+ *     rules) with s <= 32 is required.
+ *   bf_probe_red_records (timed): the add's memory traffic without hashing:
+ *     4 records per lane by one 256-bit load, Θ = s lanes per key take turns,
+ *     every lane whose word is hit issues one red.global.or in the same
+ *     instruction.  buf: b blocks of block_bits; recs 32-byte aligned. */
+int bf_probe_pattern_records(uint64_t* recs, uint64_t n, uint64_t b, uint32_t block_bits, uint32_t word_bits,
+                             uint32_t variant, uint32_t k, uint32_t z, uint64_t seed, void* stream);
+int bf_probe_red_records(void* buf, uint32_t block_bits, uint32_t word_bits, const uint64_t* recs, uint64_t n,
+                         void* stream);
 
 /* GUPS-style random-access probes (the paper's speed of light: "random
  * 64-bit loads / updates", P:L340 footnote): n accesses at addresses

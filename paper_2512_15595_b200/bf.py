@@ -60,7 +60,8 @@ _SIGS = {
     "bf_probe_read": (_i32, [_vp, _u64, _u32, _vp, _u64, _vp, _vp]),
     "bf_probe_red": (_i32, [_vp, _u64, _u32, _u32, _vp, _u64, _vp]),
     "bf_probe_rng": (_i32, [_vp, _u64, _u32, _i32, _u32, _u64, _vp]),
-    "bf_probe_red_pattern": (_i32, [_vp, _u64, _u32, _u32, _u32, _u32, _u32, _u64, _vp]),
+    "bf_probe_pattern_records": (_i32, [_vp, _u64, _u64, _u32, _u32, _u32, _u32, _u32, _u64, _vp]),
+    "bf_probe_red_records": (_i32, [_vp, _u32, _u32, _vp, _u64, _vp]),
     "bf_probe_gups": (_i32, [_vp, _u64, _u32, _i32, _i32, _u32, _u32, _u64, _vp]),
     "bf_set_l2_fetch_granularity": (_i32, [_u32]),
     "bf_set_probe_launch": (_i32, [_i32]),
@@ -279,9 +280,13 @@ def bf_probe_rng(buf, b: int, block_bits: int, red: int, lanes: int, n: int, str
     _check(_lib.bf_probe_rng(_ptr(buf), b, block_bits, red, lanes, n, _stream(stream)))
 
 
-def bf_probe_red_pattern(buf, b: int, block_bits: int, word_bits: int, variant: int, k: int, z: int, n: int,
-                         stream=None) -> None:
-    _check(_lib.bf_probe_red_pattern(_ptr(buf), b, block_bits, word_bits, variant, k, z, n, _stream(stream)))
+def bf_probe_pattern_records(recs, n: int, b: int, block_bits: int, word_bits: int, variant: int, k: int, z: int,
+                             seed: int = 0, stream=None) -> None:
+    _check(_lib.bf_probe_pattern_records(_ptr(recs), n, b, block_bits, word_bits, variant, k, z, seed, _stream(stream)))
+
+
+def bf_probe_red_records(buf, block_bits: int, word_bits: int, recs, n: int, stream=None) -> None:
+    _check(_lib.bf_probe_red_records(_ptr(buf), block_bits, word_bits, _ptr(recs), n, _stream(stream)))
 
 
 def bf_probe_gups(buf, nbytes: int, access_bytes: int, red: int, hint: int, n: int, mlp: int = 0, ctas: int = 0,

@@ -137,6 +137,8 @@ struct bf_filter {
     cudaStream_t copy_stream;
     cudaEvent_t ev_ready[2], ev_free[2];
     // binned add (HBM-resident filters, csrc/bf_binned.cuh)
+    cudaStream_t side;      // apply stream of the pipelined binned add
+    cudaEvent_t ev_bin[2], ev_apply[2];
     int add_mode;           // BF_ADD_AUTO / BF_ADD_DIRECT / BF_ADD_BINNED
     int last_add_binned;    // path the last bf_add took
     uint64_t range_bytes;   // filter bytes per bin range (0: default)
@@ -403,6 +405,11 @@ void bf_destroy(bf_filter* f)
     if (f->cursor) cudaFree(f->cursor);
     if (f->bounds) cudaFree(f->bounds);
     if (f->scratch_done) cudaEventDestroy(f->scratch_done);
+    for (int i = 0; i < 2; ++i) {
+        if (f->ev_bin[i]) cudaEventDestroy(f->ev_bin[i]);
+        if (f->ev_apply[i]) cudaEventDestroy(f->ev_apply[i]);
+    }
+    if (f->side) cudaStreamDestroy(f->side);
     cudaFree(f->words);
     delete f;
 }
@@ -512,6 +519,7 @@ static int launch_bulk(const bf_filter* f, int op, const uint64_t* keys, uint64_
 static const uint64_t kDefaultRangeBytes = 32ULL << 20;  // one L2-resident range
 static const uint64_t kDefaultMaxBatch = 1ULL << 31;     // 16 GiB of records
 static const uint64_t kBinMinFilterBytes = 96ULL << 20;  // below this the filter lives in L2
+static const uint64_t kMinBatches = 4;                    // pipelined batches of a large binned add
 
 static bool binned_available(const bf_filter* f, KernelFn* bin, KernelFn* apply)
 {
@@ -570,15 +578,27 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         ++lg;
         R = (f->b + (1ULL << lg) - 1) >> lg;
     }
-    uint64_t batch = n < (f->max_batch ? f->max_batch : kDefaultMaxBatch) ? n
-                                                                        : (f->max_batch ? f->max_batch : kDefaultMaxBatch);
+    // Batches are pipelined: batch i+1 is binned (HBM streaming, on the
+    // caller's stream) while batch i is applied (L2 atomics, on the filter's
+    // side stream), with two record buffers.  A large add is cut into at
+    // least kMinBatches batches so the two phases overlap (time ~ apply + bin
+    // / batches instead of apply + bin).
+    const uint64_t max_batch = f->max_batch ? f->max_batch : kDefaultMaxBatch;
+    uint64_t batch = n < max_batch ? n : max_batch;
+    if (!f->max_batch && n >= (kMinBatches << 24)) {
+        const uint64_t per = ((n + kMinBatches - 1) / kMinBatches + 127) & ~127ULL;
+        if (per < batch) batch = per;
+    }
     uint64_t cap = batch / R + batch / R / 32 + 8192;  // mean + 3% + slack (sd ~ sqrt(mean))
     cap = (cap + 127) & ~127ULL;
     while (R * cap >= 0xFFFFFFFFULL && batch > (1ULL << 20)) {  // record slots are u32 in the bin kernel
         batch /= 2;
         cap = ((batch / R + batch / R / 32 + 8192) + 127) & ~127ULL;
     }
-    const uint64_t need = R * cap * 8;
+    const uint64_t nbatch = (n + batch - 1) / batch;
+    const int nbuf = nbatch > 1 ? 2 : 1;
+    const uint64_t per_buf = R * cap;  // records per buffer
+    const uint64_t need = nbuf * per_buf * 8;
     cudaError_t e = cudaSuccess;
     if (f->recs_bytes < need) {
         if (f->recs) cudaFree(f->recs);
@@ -591,33 +611,48 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         }
         f->recs_bytes = need;
     }
-    if (f->cursor_n < R) {
+    if (f->cursor_n < 2 * R) {
         if (f->cursor) cudaFree(f->cursor);
         f->cursor = nullptr;
-        e = cudaMalloc(&f->cursor, R * sizeof(unsigned long long));
+        e = cudaMalloc(&f->cursor, 2 * R * sizeof(unsigned long long));
         if (e != cudaSuccess) {
             cudaGetLastError();
             return fail(BF_ENOMEM, "binned add counters: %s", cudaGetErrorString(e));
         }
-        f->cursor_n = (uint32_t)R;
+        f->cursor_n = (uint32_t)(2 * R);
+    }
+    if (!f->side) {  // the apply stream and the pipeline's events (created once per filter)
+        if ((e = cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "binned add: side stream");
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            e = cudaEventCreateWithFlags(&f->ev_bin[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&f->ev_apply[i], cudaEventDisableTiming);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "binned add: events");
     }
     const size_t smem = bin_smem_bytes((uint32_t)R, false);
     cudaFuncSetAttribute((const void*)bin_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // waves of CTAs like the bulk kernels (bin phase 178 -> 180 Gkeys/s vs the occupancy grid, tools/kexp bin2)
     const int grid_bin = kWaveCtasPerSm * sm_count(f->device);
     const int grid_apply = kWaveCtasPerSm * sm_count(f->device);
-    for (uint64_t off = 0; off < n; off += batch) {
+    cudaStream_t side = f->side;
+    uint64_t i = 0;
+    for (uint64_t off = 0; off < n; off += batch, ++i) {
+        const int buf = (int)(i & 1);
         const uint64_t cnt = n - off < batch ? n - off : batch;
         BinParams bp;
         memset(&bp, 0, sizeof bp);
         bp.f = make_params(f, keys + off, cnt, nullptr);
-        bp.recs = f->recs;
-        bp.cursor = f->cursor;
+        bp.recs = f->recs + buf * per_buf;
+        bp.cursor = f->cursor + buf * R;
         bp.cap = cap;
         bp.lg_bpr = lg;
         bp.nranges = (uint32_t)R;
         bp.range = 0;
-        if ((e = cudaMemsetAsync(f->cursor, 0, R * sizeof(unsigned long long), st)) != cudaSuccess)
+        // the buffer is free once the apply of batch i-2 has read it
+        if (i >= 2 && (e = cudaStreamWaitEvent(st, f->ev_apply[buf], 0)) != cudaSuccess)
+            return cuda_fail(e, "binned add: wait for the buffer");
+        if ((e = cudaMemsetAsync(bp.cursor, 0, R * sizeof(unsigned long long), st)) != cudaSuccess)
             return cuda_fail(e, "binned add: cursor reset");
         void* args[] = {&bp};
         uint64_t chunks = (cnt + BIN_CHUNK - 1) / BIN_CHUNK;
@@ -625,17 +660,25 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         if ((e = cudaLaunchKernel((const void*)bin_fn, dim3(gb), dim3(BIN_THREADS), args, smem, st)) != cudaSuccess)
             return cuda_fail(e, "bin launch");
         if (int rc = check_launch("bin launch")) return rc;
+        if ((e = cudaEventRecord(f->ev_bin[buf], st)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(side, f->ev_bin[buf], 0)) != cudaSuccess)
+            return cuda_fail(e, "binned add: bin -> apply");
         // one launch per range: the GPU stays inside one L2-resident range
         const uint64_t tiles = (cap + 32 * f->sched[0].kpt - 1) / (32 * f->sched[0].kpt);
         uint64_t ga = (tiles + 7) / 8;
         if (ga > (uint64_t)grid_apply) ga = grid_apply;
         for (uint32_t r = 0; r < (uint32_t)R; ++r) {
             bp.range = r;
-            if ((e = cudaLaunchKernel((const void*)apply_fn, dim3((unsigned)ga), dim3(256), args, 0, st)) != cudaSuccess)
+            if ((e = cudaLaunchKernel((const void*)apply_fn, dim3((unsigned)ga), dim3(256), args, 0, side)) != cudaSuccess)
                 return cuda_fail(e, "apply launch");
             if (int rc = check_launch("apply launch")) return rc;
         }
+        if ((e = cudaEventRecord(f->ev_apply[buf], side)) != cudaSuccess) return cuda_fail(e, "binned add: apply event");
     }
+    // join: the caller's stream continues after the last apply (the side
+    // stream runs the applies in order, so its last event covers them all)
+    if ((e = cudaStreamWaitEvent(st, f->ev_apply[(i - 1) & 1], 0)) != cudaSuccess)
+        return cuda_fail(e, "binned add: join");
     return BF_OK;
 }
 
@@ -986,21 +1029,38 @@ int bf_probe_rng(void* buf, uint64_t b, uint32_t block_bits, int red, uint32_t l
     return check_launch("probe_rng launch");
 }
 
-int bf_probe_red_pattern(void* buf, uint64_t b, uint32_t block_bits, uint32_t word_bits, uint32_t variant,
-                         uint32_t k, uint32_t z, uint64_t n, void* stream)
+int bf_probe_pattern_records(uint64_t* recs, uint64_t n, uint64_t b, uint32_t block_bits, uint32_t word_bits,
+                             uint32_t variant, uint32_t k, uint32_t z, uint64_t seed, void* stream)
 {
     if (n == 0) return BF_OK;
     uint32_t zz = 0;
-    if (!buf || b < 1 || b > (1ULL << 32) || validate(b * block_bits, k, block_bits, word_bits,
-                                                      variant == BF_CSBF ? (BF_CSBF | (z << 8)) : variant, &zz) != BF_OK ||
-        variant == BF_CBF)
-        return fail(BF_EINVAL, "bf_probe_red_pattern: bad arguments (a valid blocked configuration is required)");
+    if (!recs || ((uintptr_t)recs & 7) || b < 1 || b > (1ULL << 32) || variant == BF_CBF ||
+        validate(b * block_bits, k, block_bits, word_bits, variant == BF_CSBF ? (BF_CSBF | (z << 8)) : variant, &zz) != BF_OK)
+        return fail(BF_EINVAL, "bf_probe_pattern_records: bad arguments (a valid blocked configuration is required)");
     int dev = 0;
     cudaGetDevice(&dev);
-    if (launch_probe_red_pattern(buf, b, block_bits, word_bits, variant, k, zz, n, (cudaStream_t)stream,
-                                 g_probe_ctas_per_sm * sm_count(dev)))
-        return fail(BF_EUNSUPPORTED, "bf_probe_red_pattern: geometry outside the probe's range");
-    return check_launch("probe_red_pattern launch");
+    if (launch_pattern_records(recs, n, b, block_bits, word_bits, variant, k, zz, seed, (cudaStream_t)stream,
+                               8 * sm_count(dev)))
+        return fail(BF_EUNSUPPORTED, "bf_probe_pattern_records: more than 32 words per block");
+    return check_launch("pattern_records launch");
+}
+
+int bf_probe_red_records(void* buf, uint32_t block_bits, uint32_t word_bits, const uint64_t* recs, uint64_t n,
+                         void* stream)
+{
+    if (n == 0) return BF_OK;
+    if (!buf || !recs || ((uintptr_t)recs & 31) || (word_bits != 32 && word_bits != 64) || !is_pow2(block_bits) ||
+        block_bits < word_bits || block_bits > 1024)
+        return fail(BF_EINVAL, "bf_probe_red_records: bad arguments (records must be 32-byte aligned)");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t tiles = (n + 127) / 128;
+    uint64_t grid = (tiles + 7) / 8;
+    const uint64_t cap = (uint64_t)g_probe_ctas_per_sm * sm_count(dev);
+    if (grid > cap) grid = cap;
+    if (launch_probe_red_records(buf, block_bits, word_bits, recs, n, (cudaStream_t)stream, (int)(grid ? grid : 1)))
+        return fail(BF_EUNSUPPORTED, "bf_probe_red_records: more than 32 lanes per block");
+    return check_launch("probe_red_records launch");
 }
 
 int bf_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint32_t mlp, uint32_t ctas,

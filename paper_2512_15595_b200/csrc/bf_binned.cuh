@@ -178,8 +178,10 @@ __device__ __forceinline__ void bin_chunk(const BinParams& bp, uint64_t base, ui
         }
     }
     __syncthreads();
-    // (d) coalesced write-out of the runs
+    // (d) coalesced write-out of the runs (evict-first in L2: the pipelined
+    // apply of the previous batch keeps its filter range there)
     uint64_t* const recs = bp.recs;
+    const uint64_t pol = l2_evict_first_policy();
 #pragma unroll
     for (int i = 0; i < KPT; ++i) {
         const uint32_t j = i * NT + tid;
@@ -187,7 +189,7 @@ __device__ __forceinline__ void bin_chunk(const BinParams& bp, uint64_t base, ui
             const uint32_t d = dest[j];
             const uint64_t v = stage[j];
             if (d != 0xFFFFFFFFu) {
-                recs[d] = v;
+                st_evict_first(recs + d, v, pol);
                 if (with_idx) bp.idx_out[d] = bp.idx_base + base + stage_li[j];
             } else if (!bp.bounds) {  // bucket full: OR this key in directly (order-free)
                 add_part<C1>((W*)p.words, (uint32_t)v, (uint32_t)(v >> 32), 0, ss);

@@ -273,6 +273,19 @@ template <int PHI> struct VecLoad<32, PHI> {
     }
 };
 
+// Streaming stores that must not displace an L2-resident working set: an
+// L2 evict-first cache policy (createpolicy) on the store.
+__device__ __forceinline__ uint64_t l2_evict_first_policy()
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_evict_first(uint64_t* p, uint64_t v, uint64_t pol)
+{
+    asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+
 // red.global.or (no return value -> REDG.E.OR on sm_100a).
 __device__ __forceinline__ void red_or(uint32_t* p, uint32_t v) { atomicOr(p, v); }
 __device__ __forceinline__ void red_or(unsigned long long* p, unsigned long long v) { atomicOr(p, v); }

@@ -40,8 +40,10 @@ void launch_probe_red(void* buf, uint64_t b, uint32_t B, uint32_t lanes, const u
 
 void launch_probe_rng(const void* buf, uint64_t b, uint32_t B, int red, uint32_t lanes, uint64_t n,
                       cudaStream_t st, int grid);
-int launch_probe_red_pattern(void* buf, uint64_t b, uint32_t B, uint32_t S, uint32_t variant, uint32_t k, uint32_t z,
-                             uint64_t n, cudaStream_t st, int grid);
+int launch_pattern_records(uint64_t* recs, uint64_t n, uint64_t b, uint32_t B, uint32_t S, uint32_t variant, uint32_t k,
+                           uint32_t z, uint64_t seed, cudaStream_t st, int grid);
+int launch_probe_red_records(void* buf, uint32_t B, uint32_t S, const uint64_t* recs, uint64_t n, cudaStream_t st,
+                             int grid);
 int launch_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red, int hint, uint32_t mlp, uint64_t n,
                       cudaStream_t st, int grid);
 

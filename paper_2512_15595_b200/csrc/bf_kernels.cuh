@@ -115,6 +115,15 @@ struct Cfg {
     // (pays once the redundant work K*Θ is large: profiles/r1_bbf_csbf_sweep.md)
     static constexpr bool BBF_SMA = (V == V_BBF) && (THETA > 1) && (B >= 256) && (K * THETA >= 24) &&
                                     (BBF_SM_WORDS <= 8192);
+    // cooperative add with a TMA share (tuning::ADD_TMA_NK): the group of
+    // Θ = s lanes writes the block masks of its last TMA_NK keys per lane to
+    // shared memory and its first lane ORs each block into the filter with
+    // one cp.reduce.async.bulk (the TMA engine bypasses the L1 -> XBAR
+    // request path the red.global.or stream saturates)
+    static constexpr int TMA_NK = tuning::ADD_TMA_NK;
+    static constexpr bool TMA_ADD = TMA_NK > 0 && KPT >= TMA_NK && THETA == s && PHI == 1 && B >= 128 &&
+                                    V != V_CSBF && !BBF_SMA && HV != 3;
+    static constexpr int TMA_WORDS_PER_WARP = TMA_ADD ? 2 * 32 * TMA_NK * s : 1;  // two buffers
     using W = typename WordT<S>::T;
 
     static_assert(S == 32 || S == 64, "word size");
@@ -486,7 +495,8 @@ template <class C, bool ADD, bool FULL, bool USE_SM = true, bool KIN = false>
 __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_t lane, uint32_t pos,
                                          uint32_t gbase, bool vec_ok, const SaltSrc<C>& ss,
                                          const uint64_t (&kin)[C::KPT], uint64_t (&knext)[C::KPT],
-                                         bool have_next, uint64_t next_mine, uint32_t* sm = nullptr)
+                                         bool have_next, uint64_t next_mine, uint32_t* sm = nullptr,
+                                         uint32_t tma_buf = 0)
 {
     using W = typename C::W;
     constexpr int KPT = C::KPT;
@@ -602,6 +612,19 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
     } else {
         // (2) group-cooperative execution, one key of the group at a time
         constexpr uint32_t GMASK = (C::THETA == 32) ? 0xffffffffu : ((1u << C::THETA) - 1u);
+        constexpr bool TMA = ADD && C::TMA_ADD && USE_SM;  // (the hybrid kernel passes no staging area)
+        // TMA share: per warp and buffer, 32 * TMA_NK block slots of s words
+        // (slot (group, r, jt)) and their block indices
+        W* tslot = nullptr;
+        uint32_t* tbk = nullptr;
+        const uint32_t gslot = (lane / C::THETA) * C::THETA * C::TMA_NK;  // first slot of this group
+        if constexpr (TMA) {
+            tslot = (W*)sm + tma_buf * (32 * C::TMA_NK * C::s);
+            tbk = (uint32_t*)((W*)sm + 2 * 32 * C::TMA_NK * C::s) + tma_buf * (32 * C::TMA_NK);
+            // this buffer was last read by the bulk group committed two tiles ago
+            if (pos == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+        }
 #pragma unroll 1
         for (int r = 0; r < C::THETA; ++r) {
             const uint32_t src = gbase + r;
@@ -624,7 +647,15 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
                     v = FULL || __shfl_sync(0xffffffffu, (int)valid[j], src);
                 }
                 const Draws<C> dr(l, l2);
-                if constexpr (ADD) {
+                if constexpr (TMA) {
+                    if (j >= KPT - C::TMA_NK) {  // this key's block goes through the TMA engine
+                        const uint32_t q = gslot + (uint32_t)r * C::TMA_NK + (uint32_t)(j - (KPT - C::TMA_NK));
+                        tslot[q * C::s + pos] = v ? slot_mask<C, 0>(dr, pos, ss) : W(0);
+                        if (pos == 0) tbk[q] = v ? bk : 0xFFFFFFFFu;
+                    } else if (v) {
+                        add_part<C>((W*)p.words, dr, bk, pos, ss);
+                    }
+                } else if constexpr (ADD) {
                     if (v) add_part<C>((W*)p.words, dr, bk, pos, ss);
                 } else {
                     const W miss = v ? contains_part<C>((const W*)p.words, dr, bk, pos, ss) : W(0);
@@ -632,6 +663,30 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
                     const uint32_t ok = (((ball >> gbase) & GMASK) == 0) && v;
                     if (pos == (uint32_t)r) res |= ok << j;
                 }
+            }
+        }
+        if constexpr (TMA) {
+            // every lane's shared-memory writes -> visible to the async proxy,
+            // then the group's first lane ORs its Θ * TMA_NK blocks
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (pos == 0) {
+#pragma unroll
+                for (int q = 0; q < C::THETA * C::TMA_NK; ++q) {
+                    const uint32_t bk = tbk[gslot + q];
+                    if (bk == 0xFFFFFFFFu) continue;
+                    const uint32_t src = (uint32_t)__cvta_generic_to_shared(tslot + (gslot + q) * C::s);
+                    W* dst = (W*)p.words + (uint64_t)bk * C::s;
+                    if constexpr (C::S == 64)
+                        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.or.b64 [%0], [%1], %2;" ::"l"(dst),
+                                     "r"(src), "n"(C::B / 8)
+                                     : "memory");
+                    else
+                        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.or.b32 [%0], [%1], %2;" ::"l"(dst),
+                                     "r"(src), "n"(C::B / 8)
+                                     : "memory");
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
         }
     }
@@ -705,11 +760,18 @@ __global__ void __launch_bounds__(256, (!ADD && C::BBF_SM) ? tuning::BBF_SM_MINB
     __shared__ uint32_t s_gsalt[C::HV == 2 ? 16 : 1];
     constexpr bool SM = (C::BBF_SM && !ADD && C::THETA == 1) || (C::BBF_SMA && ADD);
     __shared__ uint32_t s_bbf[SM ? C::BBF_SM_WORDS : 1];
+    // TMA share of the cooperative add: per warp two buffers of 32 * TMA_NK
+    // block slots + their block indices (16-byte aligned slots for the bulk op)
+    constexpr bool TMA = ADD && C::TMA_ADD;
+    using W = typename C::W;
+    constexpr int TMA_WARP_BYTES = TMA ? C::TMA_WORDS_PER_WARP * (int)sizeof(W) + 2 * 32 * C::TMA_NK * 4 : 16;
+    __shared__ __align__(128) unsigned char s_tma[TMA ? 8 * TMA_WARP_BYTES : 16];
     // contains: this lane's column of its warp's KPT key slots; add: the
     // warp's staging area
-    uint32_t* const sm = !SM ? nullptr
-                             : s_bbf + (threadIdx.x >> 5) * (C::KPT * (C::B / 32) * 32) +
-                                   (ADD ? 0u : (threadIdx.x & 31u));
+    uint32_t* const sm = TMA ? (uint32_t*)(s_tma + (threadIdx.x >> 5) * TMA_WARP_BYTES)
+                     : !SM ? nullptr
+                           : s_bbf + (threadIdx.x >> 5) * (C::KPT * (C::B / 32) * 32) +
+                                 (ADD ? 0u : (threadIdx.x & 31u));
     if constexpr (C::HV == 2) {
         if (threadIdx.x < 64) s_salt[threadIdx.x] = c_salt[threadIdx.x];
         if (threadIdx.x < 16) s_gsalt[threadIdx.x] = c_gsalt[threadIdx.x];
@@ -737,7 +799,8 @@ __global__ void __launch_bounds__(256, (!ADD && C::BBF_SM) ? tuning::BBF_SM_MINB
     constexpr bool PF = ADD || C::THETA > 1 || C::PREFETCH_T1;
     uint64_t kcur[C::KPT] = {};
     if (PF && gw < nfull) load_tile_keys<C::KPT>(p.keys, gw * TILE + lane * C::KPT, vec_ok, kcur);
-    for (uint64_t t = gw; t < ntiles; t += nw) {
+    uint32_t it = 0;  // tiles done by this warp (TMA buffer parity)
+    for (uint64_t t = gw; t < ntiles; t += nw, ++it) {
         const uint64_t tn = t + nw;
         const bool have_next = tn < nfull;
         uint64_t knext[C::KPT];
@@ -748,14 +811,17 @@ __global__ void __launch_bounds__(256, (!ADD && C::BBF_SM) ? tuning::BBF_SM_MINB
         }
         if (t < nfull)
             run_tile<C, ADD, true>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
-                                   tn * TILE + lane * C::KPT, sm);
+                                   tn * TILE + lane * C::KPT, sm, it & 1u);
         else
             run_tile<C, ADD, false>(p, t, lane, pos, gbase, vec_ok, ss, kcur, knext, have_next,
-                                    tn * TILE + lane * C::KPT, sm);
+                                    tn * TILE + lane * C::KPT, sm, it & 1u);
         if constexpr (PF) {
 #pragma unroll
             for (int j = 0; j < C::KPT; ++j) kcur[j] = knext[j];
         }
+    }
+    if constexpr (TMA) {  // the bulk ops must have read shared memory before the CTA exits
+        if (pos == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
 }
 

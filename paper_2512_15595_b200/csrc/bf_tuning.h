@@ -29,5 +29,10 @@ constexpr bool TOP_MULHI = false;
 // memory allows 4 CTAs); 3 gives 80 registers, no spills: BBF 256/64 k=12
 // 133 -> 141, k=16 119 -> 125 Gkeys/s (tools/kexp)
 constexpr int BBF_SM_MINB = 3;
+// cooperative add (Θ = s): the last ADD_TMA_NK of a lane's KPT keys are ORed
+// into the filter by the TMA engine (the group writes the block's masks to
+// shared memory, its first lane issues cp.reduce.async.bulk .or), the rest by
+// red.global.or (Cfg::TMA_ADD); 0 = LSU only
+constexpr int ADD_TMA_NK = 0;
 }  // namespace tuning
 }  // namespace bf

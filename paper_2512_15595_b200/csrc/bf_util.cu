@@ -358,61 +358,111 @@ int launch_probe_gups(void* buf, uint64_t nbytes, uint32_t access_bytes, int red
     }
 }
 
-// R_red with the add's exact RED pattern but random bits (payload-matched
-// roofline of a configuration): one random block per key, a group of
-// lanes issues the REDs in one instruction as the product's add does:
-//   SBF / RBBF: s lanes, every lane ORs its word (payload B/8 per key)
-//   BBF:        s lanes, a lane ORs its word iff one of k uniform word draws
-//               hits it (payload = distinct words, s(1 - (1-1/s)^k) on
-//               average)
-//   CSBF:       z lanes, lane i ORs one uniform word of group i (payload z
-//               words)
-// Addresses and bits come from an in-register xorshift stream shared by the
-// group (no keys, no hashing).
-template <int S>
-__global__ void __launch_bounds__(256) probe_red_pattern_kernel(void* buf, uint64_t b, uint32_t s, uint32_t lgs,
-                                                                uint32_t variant, uint32_t k, uint32_t z,
-                                                                uint32_t lanes, uint64_t iters)
+// R_red with the add's exact RED pattern (payload-matched roofline of a
+// configuration).  Setup (untimed): one record per key, (block << 32) |
+// word-hit mask, with the word-hit distribution of the configuration drawn
+// from a uniform 32-bit lo by the same rules as the filter (DESIGN.md
+// section 2): SBF/RBBF every word; BBF the words hit by its k draws
+// (lo * SALT[j], top log2(B) bits); CSBF word i*g + top log2(g) bits of
+// lo * GSALT[i] for each group i.  Probe (timed): the product add's memory
+// traffic without hashing or pattern generation -- KPT = 4 records per lane
+// by one 256-bit load, Θ = s lanes per key take turns broadcasting a record
+// (two shuffles), every lane whose word is hit issues its RED in the same
+// instruction (one L2 request per key).
+__global__ void __launch_bounds__(256) pattern_records_kernel(uint64_t* recs, uint64_t n, uint64_t b, uint32_t lgB,
+                                                              uint32_t s, uint32_t lgs, uint32_t variant, uint32_t k,
+                                                              uint32_t z, uint64_t seed)
 {
-    using W = typename WordT<S>::T;
-    W* F = (W*)buf;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t pos = lane % lanes;
-    const uint64_t group = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32 + (lane - pos);
-    uint64_t x = mix64(group + 0x3c3cULL) | 1ULL;
-    const bool active = lane < (32 / lanes) * lanes;
-    for (uint64_t it = 0; it < iters; ++it) {
-        x = xs64(x);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t x = mix64(seed + i);
+        const uint32_t lo = (uint32_t)x;
         const uint64_t blk = ((x >> 32) * b) >> 32;
-        const uint64_t y = xs64(x ^ 0x9E3779B97F4A7C15ULL);
-        uint32_t w = pos;
-        bool hit = true;
-        if (variant == V_BBF) {  // k word draws of lgs bits each from y (k * lgs <= 64)
-            hit = false;
-            for (uint32_t j = 0; j < k; ++j) hit |= ((uint32_t)(y >> (j * lgs)) & (s - 1)) == pos;
+        uint32_t mask = 0;
+        if (variant == V_BBF) {
+            for (uint32_t j = 0; j < k; ++j) mask |= 1u << (((lo * c_salt[j]) >> (32 - lgB)) >> (lgB - lgs));
         } else if (variant == V_CSBF) {
             const uint32_t g = s / z;
-            w = pos * g + ((uint32_t)(y >> ((pos * 5) % 60)) & (g - 1));
+            uint32_t lgg = 0;
+            while ((1u << lgg) < g) ++lgg;
+            for (uint32_t gi = 0; gi < z; ++gi)
+                mask |= 1u << (gi * g + (lgg ? (lo * c_gsalt[gi]) >> (32 - lgg) : 0));
+        } else {
+            mask = s >= 32 ? 0xffffffffu : (1u << s) - 1;
         }
-        if (active && hit) red_or(F + blk * s + w, W(1) << ((uint32_t)(x >> (8 * (pos & 3))) & (S - 1)));
+        recs[i] = (blk << 32) | mask;
     }
 }
 
-int launch_probe_red_pattern(void* buf, uint64_t b, uint32_t B, uint32_t S, uint32_t variant, uint32_t k, uint32_t z,
-                             uint64_t n, cudaStream_t st, int grid)
+template <int S, int THETA>
+__global__ void __launch_bounds__(256) probe_red_records_kernel(void* buf, const uint64_t* recs, uint64_t n)
+{
+    using W = typename WordT<S>::T;
+    W* F = (W*)buf;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t pos = lane & (THETA - 1), gbase = lane & ~(uint32_t)(THETA - 1);
+    const uint64_t ntiles = (n + 127) / 128;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = gw; t < ntiles; t += nw) {
+        const uint64_t mine = t * 128 + lane * 4;
+        uint64_t r[4];
+        if (mine + 4 <= n) {
+            ld_keys4(recs + mine, r);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) r[j] = mine + j < n ? recs[mine + j] : 0ULL;
+        }
+#pragma unroll 1
+        for (int q = 0; q < THETA; ++q) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t m = __shfl_sync(0xffffffffu, (uint32_t)r[j], gbase + q);
+                const uint32_t bk = __shfl_sync(0xffffffffu, (uint32_t)(r[j] >> 32), gbase + q);
+                if ((m >> pos) & 1u) red_or(F + (uint64_t)bk * THETA + pos, W(1) << (bk & (S - 1)));
+            }
+        }
+    }
+}
+
+int launch_pattern_records(uint64_t* recs, uint64_t n, uint64_t b, uint32_t B, uint32_t S, uint32_t variant, uint32_t k,
+                           uint32_t z, uint64_t seed, cudaStream_t st, int grid)
 {
     const uint32_t s = B / S;
-    uint32_t lgs = 0;
+    uint32_t lgs = 0, lgB = 0;
     while ((1u << lgs) < s) ++lgs;
-    const uint32_t lanes = variant == V_CSBF ? z : s;
-    if (!lanes || lanes > 32 || (variant == V_BBF && k * lgs > 64) || (variant == V_CSBF && (s % z || (s / z) > 32)))
-        return -1;
-    const uint64_t groups = (uint64_t)grid * 256 / 32 * (32 / lanes);
-    const uint64_t iters = (n + groups - 1) / groups;
-    if (S == 64)
-        probe_red_pattern_kernel<64><<<grid, 256, 0, st>>>(buf, b, s, lgs, variant, k, z, lanes, iters);
-    else
-        probe_red_pattern_kernel<32><<<grid, 256, 0, st>>>(buf, b, s, lgs, variant, k, z, lanes, iters);
+    while ((1u << lgB) < B) ++lgB;
+    if (s > 32) return -1;
+    pattern_records_kernel<<<grid, 256, 0, st>>>(recs, n, b, lgB, s, lgs, variant, k, z, seed);
+    return 0;
+}
+
+int launch_probe_red_records(void* buf, uint32_t B, uint32_t S, const uint64_t* recs, uint64_t n, cudaStream_t st,
+                             int grid)
+{
+    const uint32_t s = B / S;
+#define BF_PRR(S_, T_) probe_red_records_kernel<S_, T_><<<grid, 256, 0, st>>>(buf, recs, n)
+    if (S == 64) {
+        switch (s) {
+        case 1: BF_PRR(64, 1); break;
+        case 2: BF_PRR(64, 2); break;
+        case 4: BF_PRR(64, 4); break;
+        case 8: BF_PRR(64, 8); break;
+        case 16: BF_PRR(64, 16); break;
+        default: return -1;
+        }
+    } else {
+        switch (s) {
+        case 1: BF_PRR(32, 1); break;
+        case 2: BF_PRR(32, 2); break;
+        case 4: BF_PRR(32, 4); break;
+        case 8: BF_PRR(32, 8); break;
+        case 16: BF_PRR(32, 16); break;
+        case 32: BF_PRR(32, 32); break;
+        default: return -1;
+        }
+    }
+#undef BF_PRR
     return 0;
 }
 

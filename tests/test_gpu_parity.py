@@ -635,7 +635,7 @@ def test_hybrid_add_matches_oracle(bflib, cuda, cfg):
     assert np.array_equal(_gpu_bytes(f), o.bytes())
 
 
-@pytest.mark.parametrize("binned", [False, True], ids=["direct", "binned"])
+@pytest.mark.parametrize("binned", [False, True, 2], ids=["direct", "binned", "binned_pipelined"])
 def test_cuda_graph_capture_and_replay(bflib, cuda, binned):
     """bf_clear + bf_add + bf_contains are stream-ordered and capture-safe:
     one captured step replayed three times gives the oracle's bits and
@@ -649,7 +649,10 @@ def test_cuda_graph_capture_and_replay(bflib, cuda, binned):
     o.add(keys)
     f = bf.Filter(1 << 22, 8, 256, 64, "SBF")
     if binned:
-        f.set_add_mode(bf.BF_ADD_BINNED, 1 << 16, 0)  # 8 ranges
+        # 8 ranges; "pipelined": 6 batches, bin of batch i+1 on the caller's
+        # stream overlapping the apply of batch i on the filter's side stream
+        # (a fork/join captured into the graph)
+        f.set_add_mode(bf.BF_ADD_BINNED, 1 << 16, 50_000 if binned == 2 else 0)
     kd = _to_dev(torch, keys, cuda)
     out = torch.empty((n + 31) // 32, dtype=torch.int32, device=cuda)
     f.add(kd)  # warm-up (lazy module loading) outside the capture
@@ -665,7 +668,7 @@ def test_cuda_graph_capture_and_replay(bflib, cuda, binned):
         out.fill_(0)
         g.replay()
     torch.cuda.synchronize()
-    assert f.add_mode()[1] == int(binned)
+    assert f.add_mode()[1] == int(bool(binned))
     assert np.array_equal(_gpu_bytes(f), o.bytes())
     assert np.array_equal(out.cpu().numpy().view(np.uint32), o.contains(keys))
 

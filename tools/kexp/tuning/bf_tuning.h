@@ -20,6 +20,9 @@
 #ifndef BF_BBF_SM_MINB
 #define BF_BBF_SM_MINB 3
 #endif
+#ifndef BF_ADD_TMA_NK
+#define BF_ADD_TMA_NK 0
+#endif
 namespace bf {
 namespace tuning {
 constexpr int T1_PF_MODE = BF_T1_PF_MODE;
@@ -28,5 +31,6 @@ constexpr bool BBF2_CLAMP = BF_BBF2_CLAMP;
 constexpr bool KEY_SMEM = BF_KEY_SMEM;
 constexpr bool TOP_MULHI = BF_TOP_MULHI;
 constexpr int BBF_SM_MINB = BF_BBF_SM_MINB;
+constexpr int ADD_TMA_NK = BF_ADD_TMA_NK;
 }  // namespace tuning
 }  // namespace bf

@@ -166,8 +166,10 @@ def row_probes(bf, torch, dev, cfg, m, keys, out, reps):
     filter's size in two launch shapes (8 and 32 CTAs per SM):
     contains -- R_read(B): one random block load per key (key-stream and
     in-register forms); add -- R_red with the add's own RED pattern
-    (bf_probe_red_pattern: s words for SBF/RBBF, the distinct words of k
-    draws for BBF, z words for CSBF, one group instruction per key)."""
+    (bf_probe_pattern_records + bf_probe_red_records: precomputed (block,
+    word-hit mask) records, s words for SBF/RBBF, the words of k draws for
+    BBF, z words for CSBF, one group instruction per key) and the generic
+    in-register block RED (all words)."""
     v, B, S, k, z = cfg
     nbytes = m // 8
     buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
@@ -191,18 +193,17 @@ def row_probes(bf, torch, dev, cfg, m, keys, out, reps):
         return min(ts)
 
     res = {}
+    recs = torch.empty(n, dtype=torch.int64, device=dev)
+    bf.bf_probe_pattern_records(recs, n, bb, B, S, v, k, z, 1)
     for cps in (8, 32):
         bf.bf_set_probe_launch(cps)
         thr = sms * cps * 256
         n_rng = -(-n // (thr * 4)) * thr * 4
-        lanes = z if v == 4 else B // S
-        groups = thr // 32 * (32 // lanes)
-        n_pat = -(-n // groups) * groups
         res[f"read_keys@{cps}"] = n / best(lambda: bf.bf_probe_read(buf, b, Bp, keys, out)) / 1e6
         res[f"read_rng@{cps}"] = n_rng / best(lambda: bf.bf_probe_rng(buf, b, Bp, 0, 1, n)) / 1e6
-        res[f"red_pattern@{cps}"] = n_pat / best(lambda: bf.bf_probe_red_pattern(buf, bb, B, S, v, k, z, n)) / 1e6
+        res[f"red_pattern@{cps}"] = n / best(lambda: bf.bf_probe_red_records(buf, B, S, recs, n)) / 1e6
     bf.bf_set_probe_launch(0)
-    del buf
+    del buf, recs
     res = {kk: round(vv, 3) for kk, vv in res.items()}
     return {"set": "c2", "variant": v, "B": B, "S": S, "k": k, "z": z, "m_bits": m, "n": n, "op": "probe",
             "read": max(vv for kk, vv in res.items() if kk.startswith("read")),
