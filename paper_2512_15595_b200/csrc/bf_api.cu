@@ -585,7 +585,7 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
     // / batches instead of apply + bin).
     const uint64_t max_batch = f->max_batch ? f->max_batch : kDefaultMaxBatch;
     uint64_t batch = n < max_batch ? n : max_batch;
-    if (!f->max_batch && n >= (kMinBatches << 24)) {
+    if (tuning::BINNED_OVERLAP && !f->max_batch && n >= (kMinBatches << 24)) {
         const uint64_t per = ((n + kMinBatches - 1) / kMinBatches + 127) & ~127ULL;
         if (per < batch) batch = per;
     }
@@ -596,7 +596,7 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         cap = ((batch / R + batch / R / 32 + 8192) + 127) & ~127ULL;
     }
     const uint64_t nbatch = (n + batch - 1) / batch;
-    const int nbuf = nbatch > 1 ? 2 : 1;
+    const int nbuf = (tuning::BINNED_OVERLAP && nbatch > 1) ? 2 : 1;  // serial phases reuse one buffer
     const uint64_t per_buf = R * cap;  // records per buffer
     const uint64_t need = nbuf * per_buf * 8;
     cudaError_t e = cudaSuccess;
@@ -621,7 +621,7 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         }
         f->cursor_n = (uint32_t)(2 * R);
     }
-    if (!f->side) {  // the apply stream and the pipeline's events (created once per filter)
+    if (tuning::BINNED_OVERLAP && !f->side) {  // the apply stream and the pipeline's events (once per filter)
         if ((e = cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking)) != cudaSuccess)
             return cuda_fail(e, "binned add: side stream");
         for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
@@ -635,10 +635,10 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
     // waves of CTAs like the bulk kernels (bin phase 178 -> 180 Gkeys/s vs the occupancy grid, tools/kexp bin2)
     const int grid_bin = kWaveCtasPerSm * sm_count(f->device);
     const int grid_apply = kWaveCtasPerSm * sm_count(f->device);
-    cudaStream_t side = f->side;
+    cudaStream_t side = tuning::BINNED_OVERLAP ? f->side : st;
     uint64_t i = 0;
     for (uint64_t off = 0; off < n; off += batch, ++i) {
-        const int buf = (int)(i & 1);
+        const int buf = nbuf == 2 ? (int)(i & 1) : 0;
         const uint64_t cnt = n - off < batch ? n - off : batch;
         BinParams bp;
         memset(&bp, 0, sizeof bp);
@@ -650,7 +650,7 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         bp.nranges = (uint32_t)R;
         bp.range = 0;
         // the buffer is free once the apply of batch i-2 has read it
-        if (i >= 2 && (e = cudaStreamWaitEvent(st, f->ev_apply[buf], 0)) != cudaSuccess)
+        if (side != st && i >= 2 && (e = cudaStreamWaitEvent(st, f->ev_apply[buf], 0)) != cudaSuccess)
             return cuda_fail(e, "binned add: wait for the buffer");
         if ((e = cudaMemsetAsync(bp.cursor, 0, R * sizeof(unsigned long long), st)) != cudaSuccess)
             return cuda_fail(e, "binned add: cursor reset");
@@ -660,8 +660,8 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         if ((e = cudaLaunchKernel((const void*)bin_fn, dim3(gb), dim3(BIN_THREADS), args, smem, st)) != cudaSuccess)
             return cuda_fail(e, "bin launch");
         if (int rc = check_launch("bin launch")) return rc;
-        if ((e = cudaEventRecord(f->ev_bin[buf], st)) != cudaSuccess ||
-            (e = cudaStreamWaitEvent(side, f->ev_bin[buf], 0)) != cudaSuccess)
+        if (side != st && ((e = cudaEventRecord(f->ev_bin[buf], st)) != cudaSuccess ||
+                           (e = cudaStreamWaitEvent(side, f->ev_bin[buf], 0)) != cudaSuccess))
             return cuda_fail(e, "binned add: bin -> apply");
         // one launch per range: the GPU stays inside one L2-resident range
         const uint64_t tiles = (cap + 32 * f->sched[0].kpt - 1) / (32 * f->sched[0].kpt);
@@ -673,11 +673,12 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
                 return cuda_fail(e, "apply launch");
             if (int rc = check_launch("apply launch")) return rc;
         }
-        if ((e = cudaEventRecord(f->ev_apply[buf], side)) != cudaSuccess) return cuda_fail(e, "binned add: apply event");
+        if (side != st && (e = cudaEventRecord(f->ev_apply[buf], side)) != cudaSuccess)
+            return cuda_fail(e, "binned add: apply event");
     }
     // join: the caller's stream continues after the last apply (the side
     // stream runs the applies in order, so its last event covers them all)
-    if ((e = cudaStreamWaitEvent(st, f->ev_apply[(i - 1) & 1], 0)) != cudaSuccess)
+    if (side != st && (e = cudaStreamWaitEvent(st, f->ev_apply[(i - 1) & 1], 0)) != cudaSuccess)
         return cuda_fail(e, "binned add: join");
     return BF_OK;
 }

@@ -101,8 +101,11 @@ struct Cfg {
     // on, staging is slower (RBBF 64 k=16 209 -> 167), and BBF blocks staged
     // in shared memory gain from it only at k >= 12 (BBF 256/64 k=8 -7%,
     // k=16 +7%: the two staging areas cost a CTA per SM)
+    // warp-specialised TMA key stream (bulk_tma_keys): contains (Θ = 1) and
+    // add, not with the shared-memory staged BBF paths (static shared memory)
+    static constexpr bool KEY_TMA_C = tuning::KEY_TMA_CONTAINS && THETA == 1 && !BBF_SM;
     static constexpr bool KEY_SMEM =
-        tuning::KEY_SMEM && THETA == 1 && KPT % 2 == 0 && !PREFETCH_T1 && (!BBF_SM || K >= 12);
+        tuning::KEY_SMEM && THETA == 1 && KPT % 2 == 0 && !PREFETCH_T1 && (!BBF_SM || K >= 12) && !KEY_TMA_C;
     static constexpr int L2PF =
         tuning::L2PF_DIST >= 0 ? tuning::L2PF_DIST : ((THETA == 1 && !PREFETCH_T1 && !BBF_SM && B <= 256) ? 2 : 0);
     // BBF add (Θ > 1) with B >= 256: each lane ORs its own keys' whole
@@ -124,6 +127,7 @@ struct Cfg {
     static constexpr bool TMA_ADD = TMA_NK > 0 && KPT >= TMA_NK && THETA == s && PHI == 1 && B >= 128 &&
                                     V != V_CSBF && !BBF_SMA && HV != 3;
     static constexpr int TMA_WORDS_PER_WARP = TMA_ADD ? 2 * 32 * TMA_NK * s : 1;  // two buffers
+    static constexpr bool KEY_TMA_A = tuning::KEY_TMA_ADD && !BBF_SMA;
     using W = typename WordT<S>::T;
 
     static_assert(S == 32 || S == 64, "word size");
@@ -753,6 +757,101 @@ __device__ __forceinline__ void contains_ksm(const Params& p, uint32_t* sm, uint
     }
 }
 
+// Warp-specialised key stream (tuning::KEY_TMA_*): warp 7 of the CTA is the
+// producer -- its lane 0 copies "super-tiles" of 7 consecutive warp tiles
+// (7 x 32 x KPT keys) into a ring of NSTAGE shared-memory stages with one
+// cp.async.bulk each (the TMA engine; completion counted on an mbarrier) --
+// and warps 0..6 consume them: wait for the stage, copy their 32 x KPT keys
+// to registers, release the stage (one arrive per warp), run the tile.  The
+// consumers' only global requests are then the random block accesses (and
+// the packed results); the key stream no longer takes L1 -> XBAR request
+// slots.  Keys must be 16-byte aligned; the tail past the last full
+// super-tile runs through the plain tile path.
+template <class C, bool ADD>
+__device__ __forceinline__ void bulk_tma_keys(const Params& p, uint32_t* sm, const uint32_t* s_salt,
+                                              const uint32_t* s_gsalt)
+{
+    constexpr int KPT = C::KPT, NCW = 7, NSTAGE = 4;
+    constexpr uint64_t TILE = 32 * KPT, SUPER = NCW * TILE;
+    __shared__ __align__(128) uint64_t s_ring[NSTAGE][SUPER];
+    __shared__ __align__(8) uint64_t s_full[NSTAGE], s_empty[NSTAGE];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < NSTAGE; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_full[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_empty[s])),
+                         "n"(NCW));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint64_t nsuper = p.n / SUPER;
+    if (warp == NCW) {  // producer
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (uint64_t c = blockIdx.x; c < nsuper; c += gridDim.x, ++it) {
+                const uint32_t s = it % NSTAGE, ph = (it / NSTAGE) & 1u;
+                const uint32_t full = (uint32_t)__cvta_generic_to_shared(&s_full[s]);
+                if (it >= NSTAGE) {  // the consumers released this stage (previous phase)
+                    const uint32_t empty = (uint32_t)__cvta_generic_to_shared(&s_empty[s]);
+                    asm volatile(
+                        "{\n\t.reg .pred P;\nWAIT_E:\n\t"
+                        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+                        "@!P bra WAIT_E;\n\t}" ::"r"(empty), "r"(ph ^ 1u) : "memory");
+                }
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full), "n"(SUPER * 8)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        (uint32_t)__cvta_generic_to_shared(&s_ring[s][0])),
+                    "l"(p.keys + c * SUPER), "n"(SUPER * 8), "r"(full)
+                    : "memory");
+            }
+        }
+        return;
+    }
+    // consumers
+    const uint32_t pos = lane & (uint32_t)(C::THETA - 1);
+    const uint32_t gbase = lane & ~(uint32_t)(C::THETA - 1);
+    SaltSrc<C> ss;
+    ss.init(pos, s_salt, s_gsalt);
+    uint32_t it = 0;
+    for (uint64_t c = blockIdx.x; c < nsuper; c += gridDim.x, ++it) {
+        const uint32_t s = it % NSTAGE, ph = (it / NSTAGE) & 1u;
+        const uint32_t full = (uint32_t)__cvta_generic_to_shared(&s_full[s]);
+        asm volatile(
+            "{\n\t.reg .pred P;\nWAIT_F:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+            "@!P bra WAIT_F;\n\t}" ::"r"(full), "r"(ph) : "memory");
+        uint64_t kin[KPT], knext[KPT];
+        const uint64_t* kb = &s_ring[s][warp * TILE + lane * KPT];
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) kin[j] = kb[j];
+        __syncwarp();
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(&s_empty[s]))
+                         : "memory");
+        run_tile<C, ADD, true, true, true>(p, c * NCW + warp, lane, pos, gbase, true, ss, kin, knext, false, 0, sm,
+                                           it & 1u);
+    }
+    // tail: whole tiles past the last super-tile, then the ragged last tile
+    const uint64_t ntiles = (p.n + TILE - 1) / TILE, nfull = p.n / TILE;
+    const uint64_t cw = (uint64_t)blockIdx.x * NCW + warp, ncw = (uint64_t)gridDim.x * NCW;
+    for (uint64_t t = nsuper * NCW + cw; t < ntiles; t += ncw, ++it) {
+        uint64_t kin[KPT] = {}, knext[KPT];
+        if (t < nfull) {
+            load_tile_keys<KPT>(p.keys, t * TILE + lane * KPT, (((uintptr_t)p.keys) & (8 * KPT - 1)) == 0, kin);
+            run_tile<C, ADD, true, true, true>(p, t, lane, pos, gbase, true, ss, kin, knext, false, 0, sm, it & 1u);
+        } else {
+            run_tile<C, ADD, false>(p, t, lane, pos, gbase, true, ss, kin, knext, false, 0, sm, it & 1u);
+        }
+    }
+    if constexpr (ADD && C::TMA_ADD) {
+        if (pos == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+}
+
 template <class C, bool ADD>
 __global__ void __launch_bounds__(256, (!ADD && C::BBF_SM) ? tuning::BBF_SM_MINB : 1) bulk_kernel(const Params p)
 {
@@ -776,6 +875,12 @@ __global__ void __launch_bounds__(256, (!ADD && C::BBF_SM) ? tuning::BBF_SM_MINB
         if (threadIdx.x < 64) s_salt[threadIdx.x] = c_salt[threadIdx.x];
         if (threadIdx.x < 16) s_gsalt[threadIdx.x] = c_gsalt[threadIdx.x];
         __syncthreads();
+    }
+    if constexpr ((ADD && C::KEY_TMA_A) || (!ADD && C::KEY_TMA_C)) {
+        if ((((uintptr_t)p.keys) & 15) == 0) {  // TMA bulk copies need 16-byte alignment
+            bulk_tma_keys<C, ADD>(p, sm, s_salt, s_gsalt);
+            return;
+        }
     }
     if constexpr (!ADD && C::KEY_SMEM) {
         __shared__ __align__(16) uint64_t s_keys[8 * 2 * 32 * C::KPT];

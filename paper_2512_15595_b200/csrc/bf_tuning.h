@@ -34,5 +34,17 @@ constexpr int BBF_SM_MINB = 3;
 // shared memory, its first lane issues cp.reduce.async.bulk .or), the rest by
 // red.global.or (Cfg::TMA_ADD); 0 = LSU only
 constexpr int ADD_TMA_NK = 0;
+// warp-specialised key stream: one warp of each CTA streams the key tiles of
+// the other seven into a shared-memory ring with TMA bulk copies
+// (cp.async.bulk + mbarriers), so key loads stop competing with the random
+// block accesses for L1 -> XBAR request slots (Cfg::KEY_TMA); per op
+constexpr bool KEY_TMA_CONTAINS = false;
+constexpr bool KEY_TMA_ADD = false;
+// binned add: pipeline the batches (bin of batch i+1 on the caller's stream
+// while batch i is applied on the filter's side stream, >= 4 batches).
+// Measured on configs[2]: 60.9 -> 66.5 ms per 2^32-key add (the bin kernel's
+// waves occupy every SM, so the apply launches only interleave with it and
+// both lose their L2 locality): off, the phases run back to back
+constexpr bool BINNED_OVERLAP = false;
 }  // namespace tuning
 }  // namespace bf

@@ -23,6 +23,12 @@
 #ifndef BF_ADD_TMA_NK
 #define BF_ADD_TMA_NK 0
 #endif
+#ifndef BF_KEY_TMA_CONTAINS
+#define BF_KEY_TMA_CONTAINS 0
+#endif
+#ifndef BF_KEY_TMA_ADD
+#define BF_KEY_TMA_ADD 0
+#endif
 namespace bf {
 namespace tuning {
 constexpr int T1_PF_MODE = BF_T1_PF_MODE;
@@ -32,5 +38,7 @@ constexpr bool KEY_SMEM = BF_KEY_SMEM;
 constexpr bool TOP_MULHI = BF_TOP_MULHI;
 constexpr int BBF_SM_MINB = BF_BBF_SM_MINB;
 constexpr int ADD_TMA_NK = BF_ADD_TMA_NK;
+constexpr bool KEY_TMA_CONTAINS = BF_KEY_TMA_CONTAINS;
+constexpr bool KEY_TMA_ADD = BF_KEY_TMA_ADD;
 }  // namespace tuning
 }  // namespace bf
