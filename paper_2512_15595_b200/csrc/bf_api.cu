@@ -766,6 +766,9 @@ int bf_contains(const bf_filter* f, const uint64_t* keys, uint64_t n, uint32_t* 
 static bool routed_kernels(const bf_filter* f, KernelFn* bin, KernelFn* apply, KernelFn* test)
 {
     if (f->variant == BF_CBF || !binned_available(f, bin, apply)) return false;
+    InstKey kr{6, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z, 1, 1, 1, 0};
+    *bin = registry_find(kr);  // the owner-binning variant
+    if (!*bin) return false;
     InstKey kt{4, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z, 1,
                (uint8_t)f->s, 1, 0};
     *test = registry_find(kt);

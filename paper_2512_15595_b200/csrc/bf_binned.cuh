@@ -127,11 +127,16 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t* a, uint32_t n
 //       consecutive threads write consecutive slots of a run.
 // Runs average CHUNK/R records (16 at R = 256 for 4096-key chunks), i.e.
 // 128-byte contiguous stores, few partial sectors at run boundaries.
-// One chunk of phase 1 (FULL: cnt == NT*KPT, no per-key bounds checks).
-template <class C1, int NT, int KPT, bool FULL>
+// One chunk of phase 1 (FULL: cnt == NT*KPT, no per-key bounds checks;
+// ROUTE: bin by owner for a partitioned filter, optional key indices,
+// records past a full bucket dropped -- else bin by range, overflow ORed in
+// directly).
+template <class C1, int NT, int KPT, bool FULL, bool ROUTE>
 __device__ __forceinline__ void bin_chunk(const BinParams& bp, uint64_t base, uint32_t cnt, uint32_t R, bool with_idx,
                                           uint64_t* stage, uint32_t* dest, uint16_t* stage_li, uint32_t* hist,
-                                          unsigned long long* gbase, uint32_t* warp_tot, const SaltSrc<C1>& ss)
+                                          unsigned long long* gbase, uint32_t* warp_tot, const SaltSrc<C1>& ss,
+                                          uint64_t* const recs, const uint64_t cap, const uint64_t seed,
+                                          const uint32_t b32, const uint32_t lg_bpr)
 {
     using W = typename C1::W;
     const Params& p = bp.f;
@@ -152,9 +157,11 @@ __device__ __forceinline__ void bin_chunk(const BinParams& bp, uint64_t base, ui
         const uint32_t li = i * NT + tid;
         rl[i] = 0xFFFFFFFFu;
         if (FULL || li < cnt) {
-            const uint64_t h = xxh64_u64(key[i], p.seed);
-            const uint32_t blk = block_of(h, p.b32);
-            const uint32_t r = bp.bounds ? owner_of(bp.bounds, R, blk) : blk >> bp.lg_bpr;
+            const uint64_t h = xxh64_u64(key[i], seed);
+            const uint32_t blk = block_of(h, b32);
+            uint32_t r;
+            if constexpr (ROUTE) r = owner_of(bp.bounds, R, blk);
+            else r = blk >> lg_bpr;
             rec[i] = ((uint64_t)blk << 32) | (uint32_t)h;
             rl[i] = (r << 16) | atomicAdd(&hist[r], 1u);
         }
@@ -165,7 +172,6 @@ __device__ __forceinline__ void bin_chunk(const BinParams& bp, uint64_t base, ui
         gbase[r] = hist[r] ? atomicAdd(&bp.cursor[r], (unsigned long long)hist[r]) : 0ULL;
     block_exclusive_scan<NT>(hist, R, warp_tot);  // hist -> run offsets in stage
     // (c) sorted slots + final destinations
-    const uint64_t cap = bp.cap;
 #pragma unroll
     for (int i = 0; i < KPT; ++i) {
         if (FULL || rl[i] != 0xFFFFFFFFu) {
@@ -174,29 +180,36 @@ __device__ __forceinline__ void bin_chunk(const BinParams& bp, uint64_t base, ui
             const unsigned long long off = gbase[r] + rank;
             stage[pos] = rec[i];
             dest[pos] = off < cap ? (uint32_t)(r * cap + off) : 0xFFFFFFFFu;
-            if (with_idx) stage_li[pos] = (uint16_t)(i * NT + tid);
+            if (ROUTE && with_idx) stage_li[pos] = (uint16_t)(i * NT + tid);
         }
     }
     __syncthreads();
-    // (d) coalesced write-out of the runs (evict-first in L2: the pipelined
-    // apply of the previous batch keeps its filter range there)
-    uint64_t* const recs = bp.recs;
+    // (d) coalesced write-out of the runs (evict-first in L2); records of a
+    // full bucket (never with uniform hashes) are handled after the loop
     const uint64_t pol = l2_evict_first_policy();
+    bool over = false;
 #pragma unroll
     for (int i = 0; i < KPT; ++i) {
         const uint32_t j = i * NT + tid;
         if (FULL || j < cnt) {
             const uint32_t d = dest[j];
-            const uint64_t v = stage[j];
             if (d != 0xFFFFFFFFu) {
-                st_evict_first(recs + d, v, pol);
-                if (with_idx) bp.idx_out[d] = bp.idx_base + base + stage_li[j];
-            } else if (!bp.bounds) {  // bucket full: OR this key in directly (order-free)
-                add_part<C1>((W*)p.words, (uint32_t)v, (uint32_t)(v >> 32), 0, ss);
-            }  // routing: dropped; the receiver sees count > cap and the host reports it
+                st_evict_first(recs + d, stage[j], pol);
+                if (ROUTE && with_idx) bp.idx_out[d] = bp.idx_base + base + stage_li[j];
+            } else {
+                over = true;
+            }
         }
     }
-    __syncthreads();
+    if (__syncthreads_or(over) && !ROUTE) {  // bucket full: OR those keys in directly (order-free)
+        for (uint32_t j = tid; j < cnt; j += NT) {
+            if (dest[j] == 0xFFFFFFFFu) {
+                const uint64_t v = stage[j];
+                add_part<C1>((W*)p.words, (uint32_t)v, (uint32_t)(v >> 32), 0, ss);
+            }
+        }
+        __syncthreads();
+    }  // routing: dropped; the receiver sees count > cap and the host reports it
 }
 
 // Phase 1.  C1 is the Θ=1 configuration of the filter (for the overflow path).
@@ -215,15 +228,16 @@ __device__ __forceinline__ void bin_chunk(const BinParams& bp, uint64_t base, ui
 //       consecutive threads write consecutive slots of a run.
 // Runs average CHUNK/R records (16 at R = 256 for 4096-key chunks), i.e.
 // 128-byte contiguous stores, few partial sectors at run boundaries.  Full
-// chunks (all but the last) run without per-key bounds checks.
-template <class C1, int NT = BIN_THREADS, int KPT = BIN_KPT>
+// chunks (all but the last) run without per-key bounds checks.  ROUTE = the
+// owner-binning of a partitioned filter (bf_route, NEXT N1).
+template <class C1, bool ROUTE, int NT = BIN_THREADS, int KPT = BIN_KPT>
 __global__ void __launch_bounds__(NT) bin_kernel(const BinParams bp)
 {
     constexpr int CHUNK = NT * KPT;
     static_assert(CHUNK <= 65536, "u16 key slots");
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t R = bp.nranges;
-    const bool with_idx = bp.idx_out != nullptr;
+    const bool with_idx = ROUTE && bp.idx_out != nullptr;
     uint64_t* stage = (uint64_t*)smem;
     uint32_t* dest = (uint32_t*)(stage + CHUNK);
     uint16_t* stage_li = (uint16_t*)(dest + CHUNK);
@@ -233,7 +247,10 @@ __global__ void __launch_bounds__(NT) bin_kernel(const BinParams bp)
 
     SaltSrc<C1> ss;
     ss.init(0, nullptr, nullptr);
-    const uint64_t n = bp.f.n;
+    // kernel parameters read once into registers
+    const uint64_t n = bp.f.n, cap = bp.cap, seed = bp.f.seed;
+    const uint32_t b32 = bp.f.b32, lg_bpr = bp.lg_bpr;
+    uint64_t* const recs = bp.recs;
     for (uint64_t c = blockIdx.x; c * CHUNK < n; c += gridDim.x) {
         const uint64_t base = c * CHUNK;
         const uint32_t cnt = (uint32_t)min((uint64_t)CHUNK, n - base);
@@ -247,10 +264,77 @@ __global__ void __launch_bounds__(NT) bin_kernel(const BinParams bp)
             }
         }
         if (cnt == CHUNK)
-            bin_chunk<C1, NT, KPT, true>(bp, base, cnt, R, with_idx, stage, dest, stage_li, hist, gbase, warp_tot, ss);
+            bin_chunk<C1, NT, KPT, true, ROUTE>(bp, base, cnt, R, with_idx, stage, dest, stage_li, hist, gbase,
+                                                warp_tot, ss, recs, cap, seed, b32, lg_bpr);
         else
-            bin_chunk<C1, NT, KPT, false>(bp, base, cnt, R, with_idx, stage, dest, stage_li, hist, gbase, warp_tot, ss);
+            bin_chunk<C1, NT, KPT, false, ROUTE>(bp, base, cnt, R, with_idx, stage, dest, stage_li, hist, gbase,
+                                                 warp_tot, ss, recs, cap, seed, b32, lg_bpr);
     }
+}
+
+// Phase 2, TMA share (tuning::APPLY_TMA_WARPS): a lane builds the whole
+// block masks of its KPT records in its shared-memory slot (double-buffered
+// per tile) and hands each block to the TMA engine with one
+// cp.reduce.async.bulk .or -- no Θ-way cooperation needed, the record
+// carries the block and lo.
+template <class C, int NTW>
+__device__ __forceinline__ void apply_tma_warp(const BinParams& bp, typename C::W* F, uint64_t r, uint64_t cnt,
+                                               uint64_t ntile, uint64_t gw, uint64_t nw, uint32_t lane)
+{
+    using W = typename C::W;
+    using C1 = Cfg<C::V, C::S, ilog2(C::s), C::K, C::Z, 1, C::s, C::KPT, 0>;  // Θ = 1 view: immediate salts
+    constexpr int KPT = C::KPT, s = C::s;
+    constexpr uint64_t TILE = 32 * KPT;
+    __shared__ __align__(128) W s_blk[NTW][2][KPT][32][s];
+    const int tw = (int)(threadIdx.x >> 5) - (8 - NTW);
+    SaltSrc<C1> ss1;
+    ss1.init(0, nullptr, nullptr);
+    uint32_t it = 0;
+    for (uint64_t lt = gw; lt < ntile; lt += nw, ++it) {
+        const uint32_t buf = it & 1u;
+        const uint64_t* rp = bp.recs + r * bp.cap + lt * TILE + (uint64_t)lane * KPT;
+        const uint64_t left = cnt - lt * TILE;
+        uint64_t rec[KPT];
+        bool valid[KPT];
+        if (left >= TILE) {
+            load_tile_keys<KPT>(rp, 0, true, rec);
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) valid[j] = true;
+        } else {
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) {
+                valid[j] = (uint64_t)lane * KPT + j < left;
+                rec[j] = valid[j] ? ld_key1(rp + j) : 0ULL;
+            }
+        }
+        // this lane's slots of this buffer were read by the bulk group committed two tiles ago
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            const Draws<C1> dr((uint32_t)rec[j]);
+            StaticFor<0, s>::run([&](auto SL) {
+                s_blk[tw][buf][j][lane][decltype(SL)::value] =
+                    slot_mask<C1, decltype(SL)::value>(dr, (uint32_t)decltype(SL)::value, ss1);
+            });
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            if (!valid[j]) continue;
+            const uint32_t src = (uint32_t)__cvta_generic_to_shared(&s_blk[tw][buf][j][lane][0]);
+            W* dst = F + (uint64_t)((uint32_t)(rec[j] >> 32) - bp.blk_base) * s;
+            if constexpr (C::S == 64)
+                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.or.b64 [%0], [%1], %2;" ::"l"(dst),
+                             "r"(src), "n"(C::B / 8)
+                             : "memory");
+            else
+                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.or.b32 [%0], [%1], %2;" ::"l"(dst),
+                             "r"(src), "n"(C::B / 8)
+                             : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // Phase 2: apply ONE bucket (bp.range) with the add schedule of C.  The host
@@ -275,6 +359,13 @@ __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
     const uint64_t r = bp.range;
     const uint64_t cnt = min((uint64_t)bp.cursor[r], bp.cap);
     const uint64_t ntile = (cnt + TILE - 1) / TILE;
+    constexpr int NTW = tuning::APPLY_TMA_WARPS;
+    if constexpr (NTW > 0 && C::B >= 128 && C::B <= 256) {  // (<= 16 KB of slots per TMA warp)
+        if ((int)(threadIdx.x >> 5) >= 8 - NTW) {  // TMA warp: whole blocks through cp.reduce.async.bulk
+            apply_tma_warp<C, NTW>(bp, F, r, cnt, ntile, gw, nw, lane);
+            return;
+        }
+    }
     for (uint64_t lt = gw; lt < ntile; lt += nw) {
         const uint64_t* rp = bp.recs + r * bp.cap + lt * TILE + (uint64_t)lane * KPT;
         const uint64_t left = cnt - lt * TILE;

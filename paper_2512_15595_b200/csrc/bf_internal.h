@@ -11,7 +11,7 @@ typedef void (*KernelFn)(Params);
 
 // Key of a specialized kernel instantiation.
 struct InstKey {
-    uint8_t op;       // 0 add, 1 contains, 2 bin, 3 apply bucket, 4 contains bucket, 5 hybrid add
+    uint8_t op;       // 0 add, 1 contains, 2 bin by range, 3 apply bucket, 4 contains bucket, 5 hybrid add, 6 bin by owner
     uint8_t variant;  // BF_BBF..BF_CSBF
     uint16_t B;
     uint8_t S, k, z, theta, phi, kpt, hv;

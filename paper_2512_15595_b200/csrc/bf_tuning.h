@@ -46,5 +46,13 @@ constexpr bool KEY_TMA_ADD = false;
 // waves occupy every SM, so the apply launches only interleave with it and
 // both lose their L2 locality): off, the phases run back to back
 constexpr bool BINNED_OVERLAP = false;
+// binned add, apply phase: the last APPLY_TMA_WARPS warps of every CTA OR
+// their records' blocks through the TMA engine (masks in shared memory,
+// cp.reduce.async.bulk), the others with the cooperative red.global.or; the
+// two paths use different request routes to the L2 (the LSU+TMA probe: +8%).
+// Measured on configs[2] (bench --config c3, same box): add 70.4 (0 warps)
+// -> 69.2 (2) -> 67.0 Gkeys/s (4): the records' block masks cost a shared-
+// memory round trip and a proxy fence per tile.  Off.
+constexpr int APPLY_TMA_WARPS = 0;
 }  // namespace tuning
 }  // namespace bf

@@ -180,7 +180,8 @@ def emit():
     binned = []
     for op, v, B, S, k, z, theta, phi, kpt, hv in inst:
         if op == 0 and (theta, phi) == default_add(v, B, S, z) and kpt == 4 and hv == 0:
-            binned.append((2, v, B, S, k, z, 1, 1, 1, 0))
+            binned.append((2, v, B, S, k, z, 1, 1, 1, 0))  # bin by range (binned add)
+            binned.append((6, v, B, S, k, z, 1, 1, 1, 0))  # bin by owner (routing, NEXT N1)
             binned.append((3, v, B, S, k, z, theta, phi, kpt, hv))
             binned.append((4, v, B, S, k, z, 1, B // S, 1, 0))  # routed contains (Θ=1, Φ=s)
             if (v, B, S, k, z) in HYBRID:
@@ -195,7 +196,9 @@ def emit():
             op, v, B, S, k, z, theta, phi, kpt, hv = i[:10]
             hs = i[10] if len(i) > 10 else 0
             if op == 2:
-                fn = f"bin_kernel<{cfg_type(i)}>"
+                fn = f"bin_kernel<{cfg_type(i)}, false>"
+            elif op == 6:
+                fn = f"bin_kernel<{cfg_type(i)}, true>"
             elif op == 3:
                 fn = f"apply_kernel<{cfg_type(i)}>"
             elif op == 4:

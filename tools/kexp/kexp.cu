@@ -210,12 +210,12 @@ static void run_binned(Ctx& c, const char* name, uint32_t range_kb, const char* 
     bp.lg_bpr = lg;
     bp.nranges = R;
     const size_t sm_bin = bin_smem_bytes(R, false, NT * BK);
-    CK(cudaFuncSetAttribute(bin_kernel<C1, NT, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bin));
+    CK(cudaFuncSetAttribute(bin_kernel<C1, false, NT, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bin));
     const size_t sm_app = (size_t)(1u << lg) * (B / 8);
     CK(cudaFuncSetAttribute(apply_smem_kernel<C1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_app));
     int nsm = 0, occ_bin = 0, occ_app = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_bin, bin_kernel<C1, NT, BK>, NT, sm_bin));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_bin, bin_kernel<C1, false, NT, BK>, NT, sm_bin));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_app, apply_smem_kernel<C1>, SMA_THREADS, sm_app));
     const uint64_t chunks = (c.n + NT * BK - 1) / (NT * BK);
     const int gb = (int)std::min<uint64_t>(chunks, (uint64_t)occ_bin * nsm);
@@ -227,7 +227,7 @@ static void run_binned(Ctx& c, const char* name, uint32_t range_kb, const char* 
     for (int r = 0; r < c.reps + 2; ++r) {
         CK(cudaEventRecord(c.e0));
         CK(cudaMemsetAsync(cursor, 0, R * 8));
-        bin_kernel<C1, NT, BK><<<gb, NT, sm_bin>>>(bp);
+        bin_kernel<C1, false, NT, BK><<<gb, NT, sm_bin>>>(bp);
         CK(cudaEventRecord(em));
         apply_smem_kernel<C1><<<ga, SMA_THREADS, sm_app>>>(bp);
         CK(cudaEventRecord(c.e1));
@@ -282,7 +282,7 @@ static void run_bin(Ctx& c, const char* name, uint32_t range_kb)
     bp.cap = cap;
     bp.lg_bpr = lg;
     bp.nranges = R;
-    auto kern = bin_kernel<C1, NT, BK>;
+    auto kern = bin_kernel<C1, false, NT, BK>;
     const size_t sm = bin_smem_bytes(R, false, NT * BK);
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int nsm = 0, occ = 0;

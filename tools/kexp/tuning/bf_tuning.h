@@ -29,6 +29,12 @@
 #ifndef BF_KEY_TMA_ADD
 #define BF_KEY_TMA_ADD 0
 #endif
+#ifndef BF_BINNED_OVERLAP
+#define BF_BINNED_OVERLAP 0
+#endif
+#ifndef BF_APPLY_TMA_WARPS
+#define BF_APPLY_TMA_WARPS 0
+#endif
 namespace bf {
 namespace tuning {
 constexpr int T1_PF_MODE = BF_T1_PF_MODE;
@@ -40,5 +46,7 @@ constexpr int BBF_SM_MINB = BF_BBF_SM_MINB;
 constexpr int ADD_TMA_NK = BF_ADD_TMA_NK;
 constexpr bool KEY_TMA_CONTAINS = BF_KEY_TMA_CONTAINS;
 constexpr bool KEY_TMA_ADD = BF_KEY_TMA_ADD;
+constexpr bool BINNED_OVERLAP = BF_BINNED_OVERLAP;
+constexpr int APPLY_TMA_WARPS = BF_APPLY_TMA_WARPS;
 }  // namespace tuning
 }  // namespace bf
