@@ -853,7 +853,8 @@ __device__ __forceinline__ void bulk_tma_keys(const Params& p, uint32_t* sm, con
 }
 
 template <class C, bool ADD>
-__global__ void __launch_bounds__(256, (!ADD && C::BBF_SM) ? tuning::BBF_SM_MINB : 1) bulk_kernel(const Params p)
+__global__ void __launch_bounds__(256, ADD ? tuning::ADD_MINB : (C::BBF_SM ? tuning::BBF_SM_MINB : tuning::CONTAINS_MINB))
+    bulk_kernel(const Params p)
 {
     __shared__ uint32_t s_salt[C::HV == 2 ? 64 : 1];
     __shared__ uint32_t s_gsalt[C::HV == 2 ? 16 : 1];

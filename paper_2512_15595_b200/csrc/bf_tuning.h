@@ -29,6 +29,15 @@ constexpr bool TOP_MULHI = false;
 // memory allows 4 CTAs); 3 gives 80 registers, no spills: BBF 256/64 k=12
 // 133 -> 141, k=16 119 -> 125 Gkeys/s (tools/kexp)
 constexpr int BBF_SM_MINB = 3;
+// minimum resident CTAs per SM requested for the other add and contains
+// kernels.  ptxas' own choice reached 150-255 registers for the BBF, RBBF
+// k >= 9 and large-k CSBF adds (one CTA per SM) and ~100 for most KPT = 4
+// contains kernels (two CTAs); 3 caps them at 80.  Measured (tools/kexp,
+// profiles/r2_kexp.md): RBBF 64 k=16 add 126 -> 190, BBF 256/64 k=16 add
+// 64 -> 84, BBF 128/64 k=8 contains 197 -> 233, SBF 256/64 k=16 contains
+// 213 -> 223 Gkeys/s; no row slower by more than 1%
+constexpr int ADD_MINB = 3;
+constexpr int CONTAINS_MINB = 3;
 // cooperative add (Θ = s): the last ADD_TMA_NK of a lane's KPT keys are ORed
 // into the filter by the TMA engine (the group writes the block's masks to
 // shared memory, its first lane issues cp.reduce.async.bulk .or), the rest by

@@ -20,6 +20,12 @@
 #ifndef BF_BBF_SM_MINB
 #define BF_BBF_SM_MINB 3
 #endif
+#ifndef BF_ADD_MINB
+#define BF_ADD_MINB 3
+#endif
+#ifndef BF_CONTAINS_MINB
+#define BF_CONTAINS_MINB 3
+#endif
 #ifndef BF_ADD_TMA_NK
 #define BF_ADD_TMA_NK 0
 #endif
@@ -44,6 +50,8 @@ constexpr bool KEY_SMEM = BF_KEY_SMEM;
 constexpr bool TOP_MULHI = BF_TOP_MULHI;
 constexpr int BBF_SM_MINB = BF_BBF_SM_MINB;
 constexpr int ADD_TMA_NK = BF_ADD_TMA_NK;
+constexpr int ADD_MINB = BF_ADD_MINB;
+constexpr int CONTAINS_MINB = BF_CONTAINS_MINB;
 constexpr bool KEY_TMA_CONTAINS = BF_KEY_TMA_CONTAINS;
 constexpr bool KEY_TMA_ADD = BF_KEY_TMA_ADD;
 constexpr bool BINNED_OVERLAP = BF_BINNED_OVERLAP;
