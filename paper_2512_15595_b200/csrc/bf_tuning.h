@@ -26,9 +26,11 @@ constexpr bool TOP_MULHI = false;
 // minimum resident CTAs per SM requested from ptxas for the BBF contains
 // kernels that stage blocks in shared memory (Cfg::BBF_SM).  ptxas' own
 // choice for them was 64 registers with spills (48 KB of static shared
-// memory allows 4 CTAs); 3 gives 80 registers, no spills: BBF 256/64 k=12
-// 133 -> 141, k=16 119 -> 125 Gkeys/s (tools/kexp)
-constexpr int BBF_SM_MINB = 3;
+// memory allows 4 CTAs); 3 gave 80 registers, no spills (BBF 256/64 k=12
+// 133 -> 141, k=16 119 -> 125 Gkeys/s); with the wave launch 4 (64
+// registers) is better again: k=12 149 -> 159, k=16 138 -> 141 (tools/kexp,
+// profiles/r2_kexp.md)
+constexpr int BBF_SM_MINB = 4;
 // minimum resident CTAs per SM requested for the other add and contains
 // kernels.  ptxas' own choice reached 150-255 registers for the BBF, RBBF
 // k >= 9 and large-k CSBF adds (one CTA per SM) and ~100 for most KPT = 4

@@ -18,7 +18,7 @@
 #define BF_TOP_MULHI 0
 #endif
 #ifndef BF_BBF_SM_MINB
-#define BF_BBF_SM_MINB 3
+#define BF_BBF_SM_MINB 4
 #endif
 #ifndef BF_ADD_MINB
 #define BF_ADD_MINB 3
