@@ -116,8 +116,8 @@ struct Cfg {
     // one access per group instead of a mask per word discarded unless selected
     static constexpr bool GROUPWISE = (V == V_CSBF) && (G > 1) && (PHI % G == 0);
     // (pays once the redundant work K*Θ is large: profiles/r1_bbf_csbf_sweep.md)
-    static constexpr bool BBF_SMA = (V == V_BBF) && (THETA > 1) && (B >= 256) && (K * THETA >= 24) &&
-                                    (BBF_SM_WORDS <= 8192);
+    static constexpr bool BBF_SMA = (V == V_BBF) && (THETA > 1) && (B >= tuning::BBF_SMA_MIN_B) &&
+                                    (K * THETA >= tuning::BBF_SMA_MIN_KT) && (BBF_SM_WORDS <= 8192);
     // cooperative add with a TMA share (tuning::ADD_TMA_NK): the group of
     // Θ = s lanes writes the block masks of its last TMA_NK keys per lane to
     // shared memory and its first lane ORs each block into the filter with

@@ -31,6 +31,12 @@ constexpr bool TOP_MULHI = false;
 // registers) is better again: k=12 149 -> 159, k=16 138 -> 141 (tools/kexp,
 // profiles/r2_kexp.md)
 constexpr int BBF_SM_MINB = 4;
+// BBF add (Θ > 1) stages each lane's whole key patterns in shared memory
+// (one shared atomic per draw) instead of every lane of the group
+// evaluating all k draws against its own word, once B >= BBF_SMA_MIN_B and
+// k * Θ >= BBF_SMA_MIN_KT (Cfg::BBF_SMA)
+constexpr int BBF_SMA_MIN_B = 256;
+constexpr int BBF_SMA_MIN_KT = 24;
 // minimum resident CTAs per SM requested for the other add and contains
 // kernels.  ptxas' own choice reached 150-255 registers for the BBF, RBBF
 // k >= 9 and large-k CSBF adds (one CTA per SM) and ~100 for most KPT = 4

@@ -20,6 +20,12 @@
 #ifndef BF_BBF_SM_MINB
 #define BF_BBF_SM_MINB 4
 #endif
+#ifndef BF_BBF_SMA_MIN_B
+#define BF_BBF_SMA_MIN_B 256
+#endif
+#ifndef BF_BBF_SMA_MIN_KT
+#define BF_BBF_SMA_MIN_KT 24
+#endif
 #ifndef BF_ADD_MINB
 #define BF_ADD_MINB 3
 #endif
@@ -51,6 +57,8 @@ constexpr bool TOP_MULHI = BF_TOP_MULHI;
 constexpr int BBF_SM_MINB = BF_BBF_SM_MINB;
 constexpr int ADD_TMA_NK = BF_ADD_TMA_NK;
 constexpr int ADD_MINB = BF_ADD_MINB;
+constexpr int BBF_SMA_MIN_B = BF_BBF_SMA_MIN_B;
+constexpr int BBF_SMA_MIN_KT = BF_BBF_SMA_MIN_KT;
 constexpr int CONTAINS_MINB = BF_CONTAINS_MINB;
 constexpr bool KEY_TMA_CONTAINS = BF_KEY_TMA_CONTAINS;
 constexpr bool KEY_TMA_ADD = BF_KEY_TMA_ADD;
