@@ -184,32 +184,24 @@ __device__ __forceinline__ void bin_chunk(const BinParams& bp, uint64_t base, ui
         }
     }
     __syncthreads();
-    // (d) coalesced write-out of the runs (evict-first in L2); records of a
-    // full bucket (never with uniform hashes) are handled after the loop
+    // (d) coalesced write-out of the runs (evict-first in L2).  No barrier
+    // after it: the next chunk writes stage/dest only after its own two
+    // barriers, and zeroes only hist, which this phase does not read.
     const uint64_t pol = l2_evict_first_policy();
-    bool over = false;
 #pragma unroll
     for (int i = 0; i < KPT; ++i) {
         const uint32_t j = i * NT + tid;
         if (FULL || j < cnt) {
             const uint32_t d = dest[j];
+            const uint64_t v = stage[j];
             if (d != 0xFFFFFFFFu) {
-                st_evict_first(recs + d, stage[j], pol);
+                st_evict_first(recs + d, v, pol);
                 if (ROUTE && with_idx) bp.idx_out[d] = bp.idx_base + base + stage_li[j];
-            } else {
-                over = true;
-            }
+            } else if (!ROUTE) {  // bucket full (never with uniform hashes): OR this key in directly
+                add_part<C1>((W*)p.words, (uint32_t)v, (uint32_t)(v >> 32), 0, ss);
+            }  // routing: dropped; the receiver sees count > cap and the host reports it
         }
     }
-    if (__syncthreads_or(over) && !ROUTE) {  // bucket full: OR those keys in directly (order-free)
-        for (uint32_t j = tid; j < cnt; j += NT) {
-            if (dest[j] == 0xFFFFFFFFu) {
-                const uint64_t v = stage[j];
-                add_part<C1>((W*)p.words, (uint32_t)v, (uint32_t)(v >> 32), 0, ss);
-            }
-        }
-        __syncthreads();
-    }  // routing: dropped; the receiver sees count > cap and the host reports it
 }
 
 // Phase 1.  C1 is the Θ=1 configuration of the filter (for the overflow path).
