@@ -185,6 +185,16 @@ class OracleFilter:
             raise ValueError("geometry-only filter has no bit array")
         return np.ctypeslib.as_array((C.c_uint8 * self.nbytes).from_address(p)).copy()
 
+    def bytes_view(self, lo: int, hi: int) -> np.ndarray:
+        """Bytes [lo, hi) of the bit array without a copy (valid while the
+        filter lives; for comparing multi-GiB filters slice by slice)."""
+        p = self._bits_ptr()
+        if not p:
+            raise ValueError("geometry-only filter has no bit array")
+        if not 0 <= lo <= hi <= self.nbytes:
+            raise ValueError("byte range outside the filter")
+        return np.ctypeslib.as_array((C.c_uint8 * (hi - lo)).from_address(p + lo))
+
     def popcount(self) -> int:
         return int(lib().bfo_popcount(self._p))
 
