@@ -630,7 +630,7 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         }
         if (e != cudaSuccess) return cuda_fail(e, "binned add: events");
     }
-    const size_t smem = bin_smem_bytes((uint32_t)R, false);
+    const size_t smem = bin_range_smem_bytes((uint32_t)R);
     cudaFuncSetAttribute((const void*)bin_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // waves of CTAs like the bulk kernels (bin phase 178 -> 180 Gkeys/s vs the occupancy grid, tools/kexp bin2)
     const int grid_bin = kWaveCtasPerSm * sm_count(f->device);

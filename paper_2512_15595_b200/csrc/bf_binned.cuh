@@ -6,7 +6,8 @@
 // order, so this path first BINS them by filter range and then applies each
 // range while it is L2-resident:
 //
-//   phase 1 (bin_kernel):   hash every key once; record = (block << 32) | lo;
+//   phase 1 (bin_range_kernel; bin_kernel for owner routing):
+//                           hash every key once; record = (block << 32) | lo;
 //                           scatter the records into per-range buckets
 //                           (CTA-local counting sort in shared memory, one
 //                           global atomic per range per CTA chunk, coalesced
@@ -49,6 +50,9 @@ struct BinParams {
 constexpr int BIN_THREADS = 512;
 constexpr int BIN_KPT = 8;
 constexpr int BIN_CHUNK = BIN_THREADS * BIN_KPT;  // keys per CTA chunk
+// resident CTAs per SM asked of ptxas for bin_range_kernel: 2 (64 registers)
+// 208-209 Gkeys/s vs 206 at 3 (40 registers + spills), tools/kexp bin3
+constexpr int BIN_RANGE_MINB = 2;
 
 // dynamic smem layout (16-byte aligned pieces):
 //   stage[CHUNK] u64 | dest[CHUNK] u32 | [li[CHUNK] u16 when routing with key
@@ -261,6 +265,225 @@ __global__ void __launch_bounds__(NT) bin_kernel(const BinParams bp)
         else
             bin_chunk<C1, NT, KPT, false, ROUTE>(bp, base, cnt, R, with_idx, stage, dest, stage_li, hist, gbase,
                                                  warp_tot, ss, recs, cap, seed, b32, lg_bpr);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Phase 1 for range binning (the binned add), round 2b.  Same records, same
+// buckets as bin_kernel<C1, false>; fewer instructions per key:
+//   * a record's bucket is a function of the record itself (range =
+//     block >> lg_bpr), so the write-out needs no per-record destination
+//     array: thread j reads stage[j], derives its range r and stores at
+//     rbase[r] + j, where rbase[r] = r * cap + reserved base - run offset
+//     (u32, one entry per bucket, computed by the bucket's owner thread in
+//     the scan step);
+//   * bucket overflow is decided per chunk (reserved base + count > cap for
+//     some bucket of the chunk, never with uniform hashes): a chunk-uniform
+//     flag selects the checked write-out;
+//   * the per-bucket counters of consecutive chunks alternate between two
+//     arrays, so no barrier is needed to zero them: chunk c zeroes the array
+//     of chunk c+1 between its own barriers;
+//   * keys are loaded 256 bits at a time (KPT consecutive keys per thread;
+//     the order of records inside a bucket run is free: OR commutes).
+// Shared memory: stage[CHUNK] u64 | cnt[2][Rp] u32 | rbase[Rp] u32 | flags.
+__host__ __device__ inline size_t bin_range_smem_bytes(uint32_t nranges, uint32_t chunk = BIN_CHUNK)
+{
+    const size_t rp = (nranges + 3) & ~3u;
+    return (size_t)chunk * 8 + rp * 4 * 3 + 16;
+}
+
+template <class C1, int NT, int KPT, bool FULL>
+__device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, uint32_t cnt, uint32_t R,
+                                                uint32_t chunk_no, uint64_t* stage, uint32_t* cnt2, uint32_t* rbase,
+                                                uint32_t* flags, uint32_t* warp_tot, const SaltSrc<C1>& ss,
+                                                uint64_t* const recs, unsigned long long* const cursor,
+                                                const uint32_t cap, const uint64_t seed, const uint32_t b32,
+                                                const uint32_t lg_bpr, const uint64_t pol)
+{
+    using W = typename C1::W;
+    constexpr int CHUNK = NT * KPT;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t Rp = (R + 3) & ~3u;
+    uint32_t* hist = cnt2 + (chunk_no & 1u) * Rp;           // this chunk's counters (zeroed by the previous chunk)
+    uint32_t* hnext = cnt2 + ((chunk_no & 1u) ^ 1u) * Rp;   // the next chunk's
+    // (a) load KPT consecutive keys, hash, rank in the bucket's counter
+    uint64_t key[KPT];
+    const uint64_t* kp = p.keys + base + (uint64_t)tid * KPT;
+    if (FULL) {
+#pragma unroll
+        for (int i = 0; i < KPT; i += 4) {
+            uint64_t k4[4];
+            ld_keys4(kp + i, k4);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) key[i + c] = k4[c];
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < KPT; ++i) key[i] = (tid * KPT + i < cnt) ? ld_key1(kp + i) : 0ULL;
+    }
+    uint64_t rec[KPT];
+    uint32_t rl[KPT];  // (bucket << 16) | rank
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) {
+        if (FULL || tid * KPT + i < cnt) {
+            const uint64_t h = xxh64_u64(key[i], seed);
+            const uint32_t blk = block_of(h, b32);
+            const uint32_t r = blk >> lg_bpr;
+            rec[i] = ((uint64_t)blk << 32) | (uint32_t)h;
+            rl[i] = (r << 16) | atomicAdd(&hist[r], 1u);
+        }
+    }
+    __syncthreads();
+    // (b) reserve each bucket's run (one global atomic per touched bucket),
+    // exclusive scan of the counts -> run offsets; rbase[r] = r*cap + base - offset
+    // Buckets per thread: one when R <= NT (the common case: every
+    // reservation of the chunk in flight at once), else ceil(R / NT)
+    // consecutive ones.  The reserved base waits in rbase[r] across the
+    // barrier.  Only the warps that own buckets scan.
+    const uint32_t per = (R + NT - 1) / NT;
+    const uint32_t r0 = tid * per, r1 = min(R, r0 + per);
+    const uint32_t nscan = (R + per * 32 - 1) / (per * 32);  // warps that own buckets
+    uint32_t tot = 0, incl = 0;
+    uint32_t c1 = 0, g1 = 0;  // per == 1: the owned bucket's count and reserved base stay in registers
+    if (per == 1) {
+        if (tid < R) {
+            c1 = hist[tid];
+            if constexpr (tuning::BIN_FAKE_RESERVE) {
+                g1 = (blockIdx.x * 16 + (chunk_no & 15u)) * 16u % (cap / 2u);
+            } else {
+                g1 = c1 ? (uint32_t)atomicAdd(cursor + tid, (unsigned long long)c1) : 0u;
+            }
+            if (g1 + c1 > cap) flags[chunk_no & 1u] = 1u;
+        }
+        if (warp < nscan) {
+            incl = c1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (uint32_t)o) incl += v;
+            }
+            if (lane == 31) warp_tot[warp] = incl;
+        }
+    } else if (warp < nscan) {
+        bool ovf = false;
+        for (uint32_t r = r0; r < r1; ++r) {
+            const uint32_t c = hist[r];
+            uint32_t g;
+            if constexpr (tuning::BIN_FAKE_RESERVE) {  // experiment: no global atomic (wrong records, timing bound)
+                g = (blockIdx.x * 16 + (chunk_no & 15u)) * 16u % (cap / 2u);
+            } else {
+                g = c ? (uint32_t)atomicAdd(cursor + r, (unsigned long long)c) : 0u;
+            }
+            rbase[r] = g;
+            ovf |= g + c > cap;
+            tot += c;
+        }
+        incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += v;
+        }
+        if (lane == 31) warp_tot[warp] = incl;
+        if (ovf) flags[chunk_no & 1u] = 1u;
+    }
+    __syncthreads();
+    if (per == 1) {
+        if (tid < R) {
+            uint32_t run = incl - c1;
+#pragma unroll
+            for (int w = 0; w < NT / 32; ++w) run += (uint32_t)w < warp ? warp_tot[w] : 0u;
+            hist[tid] = run;
+            rbase[tid] = tid * cap + g1 - run;
+            hnext[tid] = 0u;  // the next chunk's counters (last read by the previous chunk's (c))
+        }
+    } else if (warp < nscan) {
+        uint32_t run = incl - tot;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) run += (uint32_t)w < warp ? warp_tot[w] : 0u;
+        for (uint32_t r = r0; r < r1; ++r) {
+            const uint32_t c = hist[r];
+            hist[r] = run;
+            rbase[r] = r * cap + rbase[r] - run;
+            hnext[r] = 0u;  // the next chunk's counters (last read by the previous chunk's (c))
+            run += c;
+        }
+    }
+    __syncthreads();
+    // (c) sorted slots in shared memory
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) {
+        if (FULL || tid * KPT + i < cnt) stage[hist[rl[i] >> 16] + (rl[i] & 0xFFFFu)] = rec[i];
+    }
+    if (tid == 0) flags[(chunk_no & 1u) ^ 1u] = 0u;  // the next chunk's overflow flag
+    __syncthreads();
+    // (d) coalesced write-out: slot j of the chunk goes to rbase[range(stage[j])] + j
+    if (flags[chunk_no & 1u] == 0u) {
+#pragma unroll
+        for (int i = 0; i < KPT; ++i) {
+            const uint32_t j = i * NT + tid;
+            if (FULL || j < cnt) {
+                const uint64_t v = stage[j];
+                st_evict_first(recs + (rbase[(uint32_t)(v >> 32) >> lg_bpr] + j), v, pol);
+            }
+        }
+    } else {  // some bucket of this chunk is full (never with uniform hashes): OR its overflow directly
+#pragma unroll 1
+        for (int i = 0; i < KPT; ++i) {
+            const uint32_t j = i * NT + tid;
+            if (FULL || j < cnt) {
+                const uint64_t v = stage[j];
+                const uint32_t r = (uint32_t)(v >> 32) >> lg_bpr;
+                const uint32_t d = rbase[r] + j;
+                if (d - r * cap < cap) st_evict_first(recs + d, v, pol);
+                else add_part<C1>((W*)p.words, (uint32_t)v, (uint32_t)(v >> 32), 0, ss);
+            }
+        }
+    }
+}
+
+template <class C1, int NT = BIN_THREADS, int KPT = BIN_KPT, int MINB = BIN_RANGE_MINB>
+__global__ void __launch_bounds__(NT, MINB) bin_range_kernel(const BinParams bp)
+{
+    constexpr int CHUNK = NT * KPT;
+    static_assert(CHUNK <= 65536 && KPT % 4 == 0, "u16 ranks, 256-bit key loads");
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t R = bp.nranges;
+    const uint32_t Rp = (R + 3) & ~3u;
+    uint64_t* stage = (uint64_t*)smem;
+    uint32_t* cnt2 = (uint32_t*)(stage + CHUNK);
+    uint32_t* rbase = cnt2 + 2 * Rp;
+    uint32_t* flags = rbase + Rp;
+    __shared__ uint32_t warp_tot[NT / 32];
+    for (uint32_t r = threadIdx.x; r < Rp; r += NT) cnt2[r] = 0u;
+    if (threadIdx.x < 2) flags[threadIdx.x] = 0u;
+    __syncthreads();
+    SaltSrc<C1> ss;
+    ss.init(0, nullptr, nullptr);
+    const Params p = bp.f;
+    const uint64_t n = p.n, seed = p.seed;
+    const uint32_t cap = (uint32_t)bp.cap, b32 = p.b32, lg_bpr = bp.lg_bpr;
+    uint64_t* const recs = bp.recs;
+    unsigned long long* const cursor = bp.cursor;
+    const uint64_t pol = l2_evict_first_policy();
+    const bool vec_ok = ((uintptr_t)p.keys & 31u) == 0;
+    uint32_t chunk_no = 0;
+    for (uint64_t c = blockIdx.x; c * CHUNK < n; c += gridDim.x, ++chunk_no) {
+        const uint64_t base = c * CHUNK;
+        const uint32_t cnt = (uint32_t)min((uint64_t)CHUNK, n - base);
+        {  // L2 prefetch of this CTA's next chunk (one grid stride ahead)
+            const uint64_t pb = base + (uint64_t)gridDim.x * CHUNK;
+            for (uint32_t l = threadIdx.x; l < CHUNK / 16; l += NT) {
+                const uint64_t q = pb + (uint64_t)l * 16;
+                if (q < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.keys + q));
+            }
+        }
+        if (cnt == CHUNK && vec_ok)
+            bin_range_chunk<C1, NT, KPT, true>(p, base, cnt, R, chunk_no, stage, cnt2, rbase, flags, warp_tot, ss,
+                                               recs, cursor, cap, seed, b32, lg_bpr, pol);
+        else
+            bin_range_chunk<C1, NT, KPT, false>(p, base, cnt, R, chunk_no, stage, cnt2, rbase, flags, warp_tot, ss,
+                                                recs, cursor, cap, seed, b32, lg_bpr, pol);
     }
 }
 

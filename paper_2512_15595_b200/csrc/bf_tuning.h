@@ -71,5 +71,8 @@ constexpr bool BINNED_OVERLAP = false;
 // -> 69.2 (2) -> 67.0 Gkeys/s (4): the records' block masks cost a shared-
 // memory round trip and a proxy fence per tile.  Off.
 constexpr int APPLY_TMA_WARPS = 0;
+// experiment only (tools/kexp): the bin kernel's per-chunk run reservation
+// without the global atomic -- a timing bound, the records land in wrong slots
+constexpr bool BIN_FAKE_RESERVE = false;
 }  // namespace tuning
 }  // namespace bf

@@ -196,7 +196,7 @@ def emit():
             op, v, B, S, k, z, theta, phi, kpt, hv = i[:10]
             hs = i[10] if len(i) > 10 else 0
             if op == 2:
-                fn = f"bin_kernel<{cfg_type(i)}, false>"
+                fn = f"bin_range_kernel<{cfg_type(i)}>"
             elif op == 6:
                 fn = f"bin_kernel<{cfg_type(i)}, true>"
             elif op == 3:

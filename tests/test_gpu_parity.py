@@ -349,11 +349,14 @@ BINNED_CFGS = [(3, 256, 64, 8, 0), (1, 256, 64, 8, 0), (4, 256, 32, 8, 4), (2, 6
 
 
 @pytest.mark.parametrize("cfg", BINNED_CFGS)
-@pytest.mark.parametrize("range_bytes,batch", [(1 << 16, 0), (1 << 15, 30_000), (3 << 14, 7_777)])
-def test_binned_add_matches_oracle(bflib, cuda, cfg, range_bytes, batch):
+@pytest.mark.parametrize("range_bytes,batch,misalign", [(1 << 16, 0, 0), (1 << 15, 30_000, 0), (3 << 14, 7_777, 0),
+                                                         (1 << 10, 0, 0), (1 << 16, 0, 1)])
+def test_binned_add_matches_oracle(bflib, cuda, cfg, range_bytes, batch, misalign):
     """BF_ADD_BINNED (hash once, bin by filter range, apply range-major) builds
     exactly the oracle's filter, across several ranges, batches and a ragged
-    last range."""
+    last range; 1 KiB ranges give R > 512 buckets (several per bin-kernel
+    thread); misalign = keys 8 bytes off a 32-byte boundary (the bin kernel's
+    scalar key path)."""
     import torch
     bf = bflib
     v, B, S, k, z = cfg
@@ -363,7 +366,12 @@ def test_binned_add_matches_oracle(bflib, cuda, cfg, range_bytes, batch):
     o.add(keys)
     f = bf.Filter(m, k, B, S, variant=v, z=z)
     f.set_add_mode(bf.BF_ADD_BINNED, range_bytes, batch)
-    f.add(_to_dev(torch, keys, cuda))
+    if misalign:
+        kd = torch.empty(keys.size + 1, dtype=torch.int64, device=cuda)
+        kd[1:].copy_(_to_dev(torch, keys, cuda))
+        f.add(kd[1:])
+    else:
+        f.add(_to_dev(torch, keys, cuda))
     torch.cuda.synchronize()
     assert f.add_mode() == (bf.BF_ADD_BINNED, 1)
     assert np.array_equal(_gpu_bytes(f), o.bytes())

@@ -253,7 +253,7 @@ static void run_binned(Ctx& c, const char* name, uint32_t range_kb, const char* 
 }
 
 // bin phase only (records into R buckets), staged vs register-direct writes
-template <class C1, int NT, int BK, bool REG>
+template <class C1, int NT, int BK, bool REG, bool V2 = false, int MINB = 2>
 static void run_bin(Ctx& c, const char* name, uint32_t range_kb)
 {
     const uint64_t B = C1::B;
@@ -282,8 +282,8 @@ static void run_bin(Ctx& c, const char* name, uint32_t range_kb)
     bp.cap = cap;
     bp.lg_bpr = lg;
     bp.nranges = R;
-    auto kern = bin_kernel<C1, false, NT, BK>;
-    const size_t sm = bin_smem_bytes(R, false, NT * BK);
+    auto kern = V2 ? bin_range_kernel<C1, NT, BK, MINB> : bin_kernel<C1, false, NT, BK>;
+    const size_t sm = V2 ? bin_range_smem_bytes(R, NT * BK) : bin_smem_bytes(R, false, NT * BK);
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int nsm = 0, occ = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
@@ -318,7 +318,7 @@ static void run_bin(Ctx& c, const char* name, uint32_t range_kb)
     std::sort(ts.begin(), ts.end());
     printf("{\"cfg\": \"%s\", \"bin\": \"%s\", \"nt\": %d, \"bk\": %d, \"R\": %u, \"occ\": %d, \"grid\": %d, \"bin_ms\": %.4f, "
            "\"gkeys_s\": %.2f, \"total\": %llu, \"xor\": \"%016llx\"}\n",
-           name, REG ? "reg" : "staged", NT, BK, R, occ, gb, ts[ts.size() / 2], c.n / ts[ts.size() / 2] / 1e6,
+           name, V2 ? (MINB == 1 ? "v2m1" : MINB == 2 ? "v2m2" : MINB == 3 ? "v2m3" : MINB == 4 ? "v2m4" : "v2m6") : (REG ? "reg" : "staged"), NT, BK, R, occ, gb, ts[ts.size() / 2], c.n / ts[ts.size() / 2] / 1e6,
            (unsigned long long)tot, (unsigned long long)x);
     fflush(stdout);
     (void)sum;
@@ -445,6 +445,32 @@ int main(int argc, char** argv)
             run_bin<SBF8, 256, 12, false>(c, "SBF256/64 k8", 128);
             run_bin<SBF8, 512, 16, false>(c, "SBF256/64 k8", 128);
             run_bin<SBF8, 1024, 8, false>(c, "SBF256/64 k8", 128);
+        }
+        return 0;
+    }
+    if (argc > 1 && strcmp(argv[1], "binp") == 0) {  // the product bin kernel only (ncu target)
+        using SBF8 = Cfg<V_SBF, 64, 2, 8, 0, 1, 4, 1, 0>;
+        run_bin<SBF8, BIN_THREADS, BIN_KPT, false>(c, "SBF256/64 k8", 128);
+        return 0;
+    }
+    if (argc > 1 && strcmp(argv[1], "bin4") == 0) {  // ncu pair: r2 kernel vs range v2, 512 x 8
+        using SBF8 = Cfg<V_SBF, 64, 2, 8, 0, 1, 4, 1, 0>;
+        c.reps = 1;
+        run_bin<SBF8, 512, 8, false>(c, "SBF256/64 k8", 128);
+        run_bin<SBF8, 512, 8, false, true, 2>(c, "SBF256/64 k8", 128);
+        return 0;
+    }
+    if (argc > 1 && strcmp(argv[1], "bin3") == 0) {  // range binning v2 vs the r2 kernel, R = 256
+        using SBF8 = Cfg<V_SBF, 64, 2, 8, 0, 1, 4, 1, 0>;
+        for (int rep = 0; rep < 2; ++rep) {
+            run_bin<SBF8, 512, 8, false>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 512, 8, false, true, 2>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 512, 8, false, true, 3>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 256, 8, false, true, 4>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 256, 16, false, true, 4>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 512, 16, false, true, 2>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 1024, 8, false, true, 1>(c, "SBF256/64 k8", 128);
+            run_bin<SBF8, 1024, 4, false, true, 2>(c, "SBF256/64 k8", 128);
         }
         return 0;
     }

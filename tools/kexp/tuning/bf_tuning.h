@@ -64,5 +64,9 @@ constexpr bool KEY_TMA_CONTAINS = BF_KEY_TMA_CONTAINS;
 constexpr bool KEY_TMA_ADD = BF_KEY_TMA_ADD;
 constexpr bool BINNED_OVERLAP = BF_BINNED_OVERLAP;
 constexpr int APPLY_TMA_WARPS = BF_APPLY_TMA_WARPS;
+#ifndef BF_BIN_FAKE_RESERVE
+#define BF_BIN_FAKE_RESERVE 0
+#endif
+constexpr bool BIN_FAKE_RESERVE = BF_BIN_FAKE_RESERVE;
 }  // namespace tuning
 }  // namespace bf
