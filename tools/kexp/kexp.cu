@@ -328,8 +328,9 @@ int main(int argc, char** argv)
 {
     Ctx c{};
     c.m_bits = 1ULL << 28;
-    c.n = 1ULL << 26;
+    c.n = getenv("KEXP_N") ? strtoull(getenv("KEXP_N"), nullptr, 0) : 1ULL << 26;
     c.reps = 9;
+
     CK(cudaMalloc(&c.words, c.m_bits / 8));
     CK(cudaMalloc(&c.keys, c.n * 8));
     CK(cudaMalloc(&c.neg, c.n * 8));
