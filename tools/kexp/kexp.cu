@@ -324,6 +324,79 @@ static void run_bin(Ctx& c, const char* name, uint32_t range_kb)
     (void)sum;
 }
 
+
+// ---- clear experiments (32 MiB L2-resident, dirty): memset vs store kernels vs TMA bulk stores
+__global__ void clear_st128(uint4* p, uint64_t n16)
+{
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = make_uint4(0, 0, 0, 0);
+}
+__global__ void clear_st256(uint32_t* p, uint64_t n32)
+{
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n32; i += (uint64_t)gridDim.x * blockDim.x)
+        asm volatile("st.global.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p + 8 * i), "r"(0) : "memory");
+}
+__global__ void clear_tma(unsigned char* p, uint64_t nbytes)
+{
+    __shared__ __align__(128) unsigned char z[16384];
+    for (int i = threadIdx.x; i < 16384 / 16; i += blockDim.x) ((uint4*)z)[i] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint64_t off = (uint64_t)blockIdx.x * 16384; off < nbytes; off += (uint64_t)gridDim.x * 16384)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 16384;" ::"l"(p + off),
+                         "r"((uint32_t)__cvta_generic_to_shared(z)) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+}
+__global__ void dirty(uint32_t* p, uint64_t n4)
+{
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += (uint64_t)gridDim.x * blockDim.x)
+        atomicOr(p + i, 1u);
+}
+static void run_clear(Ctx& c)
+{
+    const uint64_t nb = c.m_bits / 8;
+    int nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+    auto timeit = [&](const char* name, auto fn) {
+        std::vector<float> ts;
+        for (int r = 0; r < 12; ++r) {
+            dirty<<<nsm * 8, 256>>>((uint32_t*)c.words, nb / 4);
+            CK(cudaEventRecord(c.e0));
+            fn();
+            CK(cudaEventRecord(c.e1));
+            CK(cudaEventSynchronize(c.e1));
+            CK(cudaGetLastError());
+            float ms;
+            CK(cudaEventElapsedTime(&ms, c.e0, c.e1));
+            if (r >= 2) ts.push_back(ms);
+        }
+        std::sort(ts.begin(), ts.end());
+        std::vector<unsigned char> h(nb);
+        CK(cudaMemcpy(h.data(), c.words, nb, cudaMemcpyDeviceToHost));
+        bool zero = true;
+        for (size_t i = 0; i < nb; ++i) zero &= h[i] == 0;
+        printf("{\"clear\": \"%s\", \"bytes\": %llu, \"us\": %.2f, \"gb_s\": %.0f, \"zero\": %s}\n", name,
+               (unsigned long long)nb, ts[ts.size() / 2] * 1e3, nb / (ts[ts.size() / 2] * 1e-3) / 1e9, zero ? "true" : "false");
+        fflush(stdout);
+    };
+    timeit("memset", [&] { CK(cudaMemsetAsync(c.words, 0, nb)); });
+    for (int cps : {4, 8, 16}) {
+        char nm[64];
+        snprintf(nm, sizeof nm, "st128@%d", cps);
+        timeit(nm, [&] { clear_st128<<<nsm * cps, 256>>>((uint4*)c.words, nb / 16); });
+        snprintf(nm, sizeof nm, "st256@%d", cps);
+        timeit(nm, [&] { clear_st256<<<nsm * cps, 256>>>((uint32_t*)c.words, nb / 32); });
+    }
+    for (int g : {148, 296, 592, 1184, 2048}) {
+        char nm[64];
+        snprintf(nm, sizeof nm, "tma@%d", g);
+        timeit(nm, [&] { clear_tma<<<g, 128>>>((unsigned char*)c.words, nb); });
+    }
+}
+
 int main(int argc, char** argv)
 {
     Ctx c{};
@@ -340,6 +413,10 @@ int main(int argc, char** argv)
     CK(cudaDeviceSynchronize());
     CK(cudaEventCreate(&c.e0));
     CK(cudaEventCreate(&c.e1));
+    if (argc > 1 && strcmp(argv[1], "clear") == 0) {
+        run_clear(c);
+        return 0;
+    }
     if (argc > 1 && strcmp(argv[1], "bbf128") == 0) {
         run<Cfg<V_BBF, 64, 1, 4, 0, 2, 1, 4, 0>, Cfg<V_BBF, 64, 1, 4, 0, 1, 2, 4, 0>>(c, "BBF128/64 k4");
         run<Cfg<V_BBF, 64, 1, 6, 0, 2, 1, 4, 0>, Cfg<V_BBF, 64, 1, 6, 0, 1, 2, 4, 0>>(c, "BBF128/64 k6");
