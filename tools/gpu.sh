@@ -6,6 +6,7 @@
 #   launches  ncu launch list (gpu__time_duration per launch) of the default bench command
 #   prof      ncu --set full of the bench's bulk kernels (extra args go to bench.py)
 #   sanitize  compute-sanitizer memcheck / racecheck / synccheck over tools/sanitize_run.py
+#   profbin   ncu --set full of the binned add's bin + apply kernels (configs[2], one 2^31-key batch)
 # Everything lands in gpurun_out/ with the TAG in its name.
 set -u
 JOB=${1:-suite}
@@ -33,6 +34,12 @@ prof)
     -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-probe --no-graph --no-hbm --no-fixed "$@" \
     > gpurun_out/prof_$TAG.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/prof_$TAG.log
+  ;;
+profbin)
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"bin_range_kernel|apply_kernel" -c 2 \
+    -o gpurun_out/profbin_$TAG python bench.py --config c3 --steps 1 --warmup 0 --no-e2e --no-cpu --no-probe --no-graph "$@" \
+    > gpurun_out/profbin_$TAG.log 2>&1
+  echo "ncu rc=$?" >> gpurun_out/profbin_$TAG.log
   ;;
 sanitize)
   for tool in memcheck racecheck synccheck; do
