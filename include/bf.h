@@ -188,6 +188,32 @@ int bf_set_add_mode(bf_filter* f, int mode, uint64_t range_bytes, uint64_t max_b
 /* mode set by bf_set_add_mode, and whether the most recent bf_add was binned. */
 int bf_get_add_mode(const bf_filter* f, int* mode, int* last_binned);
 
+/* Bulk-contains strategy for filters larger than L2 (HBM-resident; round 2b).
+ *   BF_CONTAINS_DIRECT  every key's block is loaded straight from the filter
+ *                       (one random HBM block read per key: the paper's
+ *                       GUPS-bound regime).
+ *   BF_CONTAINS_BINNED  the lookup counterpart of BF_ADD_BINNED: keys are
+ *                       hashed once and binned by filter range (record =
+ *                       block, low hash word) together with each key's record
+ *                       slot; every range is then tested while it is
+ *                       L2-resident (one result bit per record slot) and the
+ *                       bits are gathered back into key order.  Same answers
+ *                       (a key's answer depends only on its block and
+ *                       pattern).  Uses the range size and batch limit
+ *                       of bf_set_add_mode and the same filter-owned scratch
+ *                       (+ 4 bytes per key of a batch for the slots and one
+ *                       bit per record slot), serialised with the binned add
+ *                       the same way.
+ *   BF_CONTAINS_AUTO    binned when the filter is >= 96 MiB and the call has
+ *                       at least one key per filter block (n >= b; default),
+ *                       i.e. when a range's lines serve several keys.
+ * BF_EUNSUPPORTED if the binned kernels are not compiled for this
+ * configuration (or a non-default draw scheme). */
+enum { BF_CONTAINS_AUTO = 0, BF_CONTAINS_DIRECT = 1, BF_CONTAINS_BINNED = 2 };
+int bf_set_contains_mode(bf_filter* f, int mode);
+/* mode set by bf_set_contains_mode, and whether the most recent bf_contains was binned. */
+int bf_get_contains_mode(const bf_filter* f, int* mode, int* last_binned);
+
 /* Current schedule of `op` and whether it runs a specialized (compile-time
  * k/B/S) kernel (1) or the generic runtime-parameter kernel (0). */
 int bf_get_layout(const bf_filter* f, int op, int* theta, int* phi, int* kpt,

@@ -68,6 +68,8 @@ _SIGS = {
     "bf_get_l2_fetch_granularity": (_i32, [C.POINTER(_u32)]),
     "bf_set_add_mode": (_i32, [_vp, _i32, _u64, _u64]),
     "bf_get_add_mode": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
+    "bf_set_contains_mode": (_i32, [_vp, _i32]),
+    "bf_get_contains_mode": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
     "bf_create_part": (_vp, [_u64, _u32, _u32, _u32, _u32, _u64, _u32, _u32]),
     "bf_part_info": (_i32, [_vp, C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u64), C.POINTER(_u64),
                             C.POINTER(_u64)]),
@@ -255,6 +257,19 @@ def bf_get_add_mode(f: int) -> tuple[int, int]:
     m, last = _i32(), _i32()
     _check(_lib.bf_get_add_mode(f, C.byref(m), C.byref(last)))
     return int(m.value), int(last.value)
+
+
+BF_CONTAINS_AUTO, BF_CONTAINS_DIRECT, BF_CONTAINS_BINNED = 0, 1, 2
+
+
+def bf_set_contains_mode(f: int, mode: int) -> None:
+    _check(_lib.bf_set_contains_mode(f, mode))
+
+
+def bf_get_contains_mode(f: int) -> tuple[int, int]:
+    m, last = C.c_int(0), C.c_int(0)
+    _check(_lib.bf_get_contains_mode(f, C.byref(m), C.byref(last)))
+    return m.value, last.value
 
 
 def bf_or_fold(dst, srcs, nsrc: int, src_stride_bytes: int, nbytes: int, stream=None) -> None:
@@ -480,6 +495,13 @@ class Filter:
 
     def set_add_mode(self, mode: int, range_bytes: int = 0, max_batch_keys: int = 0):
         bf_set_add_mode(self.handle, mode, range_bytes, max_batch_keys)
+
+    def set_contains_mode(self, mode: int):
+        bf_set_contains_mode(self.handle, mode)
+
+    def contains_mode(self) -> tuple[int, int]:
+        """(mode, whether the last contains took the binned path)."""
+        return bf_get_contains_mode(self.handle)
 
     def add_mode(self) -> tuple[int, int]:
         """(mode, whether the last add took the binned path)."""

@@ -147,6 +147,15 @@ struct bf_filter {
     uint64_t recs_bytes;
     unsigned long long* cursor;
     uint32_t cursor_n;
+    // binned contains (round 2b): the keys' record slots and the per-slot
+    // result bits of one batch; mode and last path (mutable: bf_contains
+    // takes a const filter, the scratch is not part of its state)
+    uint32_t* slots;
+    uint64_t slots_bytes;
+    uint32_t* resb;
+    uint64_t resb_bytes;
+    int contains_mode;         // BF_CONTAINS_AUTO / _DIRECT / _BINNED
+    int last_contains_binned;
     // block-range partition (NEXT N1): this filter holds global blocks
     // [blk_lo, blk_hi) of a b_global-block filter split over nparts owners
     uint32_t nparts, part;
@@ -403,6 +412,8 @@ void bf_destroy(bf_filter* f)
     free_staging(f);
     if (f->recs) cudaFree(f->recs);
     if (f->cursor) cudaFree(f->cursor);
+    if (f->slots) cudaFree(f->slots);
+    if (f->resb) cudaFree(f->resb);
     if (f->bounds) cudaFree(f->bounds);
     if (f->scratch_done) cudaEventDestroy(f->scratch_done);
     for (int i = 0; i < 2; ++i) {
@@ -683,6 +694,137 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
     return BF_OK;
 }
 
+// ------------------------------------------------------------ binned contains
+// The lookup counterpart of the binned add (csrc/bf_binned.cuh): bin the
+// queries by filter range (keeping every key's record slot), test each range
+// while it is L2-resident (one launch per range), gather the result bits back
+// into key order.  Same answers as the direct kernel.
+static bool binned_contains_available(const bf_filter* f, KernelFn* bin, KernelFn* look, KernelFn* unbin)
+{
+    if (f->variant == BF_CBF || f->scheme != 0 || f->nparts > 1) return false;  // records carry lo only
+    InstKey kb{7, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z, 1, 1, 1, 0};
+    InstKey kl{8, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z, 1,
+               (uint8_t)(f->B / f->S), 1, 0};
+    InstKey ku{9, (uint8_t)f->variant, (uint16_t)f->B, (uint8_t)f->S, (uint8_t)f->k, (uint8_t)f->z, 1,
+               (uint8_t)(f->B / f->S), 1, 0};
+    *bin = registry_find(kb);
+    *look = registry_find(kl);
+    *unbin = registry_find(ku);
+    return *bin && *look && *unbin;
+}
+
+static int ensure_scratch(void** p, uint64_t* have, uint64_t need, const char* what)
+{
+    if (*have >= need) return BF_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+    cudaError_t e = cudaMalloc(p, need);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(BF_ENOMEM, "%s (%llu bytes): %s", what, (unsigned long long)need, cudaGetErrorString(e));
+    }
+    *have = need;
+    return BF_OK;
+}
+
+static int binned_contains_locked(bf_filter* f, const uint64_t* keys, uint64_t n, uint32_t* out, cudaStream_t st,
+                                  KernelFn bin_fn, KernelFn look_fn, KernelFn unbin_fn)
+{
+    const uint64_t blk_bytes = f->B / 8;
+    uint64_t range_bytes = f->range_bytes ? f->range_bytes
+                                          : (n * 8 < f->bytes ? 2 * kDefaultRangeBytes : kDefaultRangeBytes);
+    uint32_t lg = 0;
+    while ((blk_bytes << (lg + 1)) <= range_bytes) ++lg;  // blocks per range = 2^lg
+    uint64_t R = (f->b + (1ULL << lg) - 1) >> lg;
+    while (R > 4096) {
+        ++lg;
+        R = (f->b + (1ULL << lg) - 1) >> lg;
+    }
+    // batches: whole result words (multiples of 128 keys) except the last
+    const uint64_t max_batch = f->max_batch ? f->max_batch : kDefaultMaxBatch;
+    uint64_t batch = n <= max_batch ? n : (max_batch & ~127ULL ? max_batch & ~127ULL : 128);
+    uint64_t cap = ((batch / R + batch / R / 32 + 8192) + 127) & ~127ULL;
+    while (R * cap >= 0xFFFFFFFEULL && batch > (1ULL << 20)) {  // slots are u32; 0xFFFFFFFE/F are markers
+        batch = (batch / 2) & ~127ULL;
+        cap = ((batch / R + batch / R / 32 + 8192) + 127) & ~127ULL;
+    }
+    int rc;
+    if ((rc = ensure_scratch((void**)&f->recs, &f->recs_bytes, R * cap * 8, "binned contains records")) != BF_OK) return rc;
+    if ((rc = ensure_scratch((void**)&f->slots, &f->slots_bytes, batch * 4, "binned contains key slots")) != BF_OK) return rc;
+    if ((rc = ensure_scratch((void**)&f->resb, &f->resb_bytes, R * cap / 8, "binned contains result bits")) != BF_OK) return rc;
+    if (f->cursor_n < 2 * R) {
+        uint64_t have = (uint64_t)f->cursor_n * sizeof(unsigned long long);
+        if ((rc = ensure_scratch((void**)&f->cursor, &have, 2 * R * sizeof(unsigned long long), "binned counters")) != BF_OK)
+            return rc;
+        f->cursor_n = (uint32_t)(2 * R);
+    }
+    cudaError_t e;
+    const size_t smem = bin_range_smem_bytes((uint32_t)R);
+    cudaFuncSetAttribute((const void*)bin_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int waves = kWaveCtasPerSm * sm_count(f->device);
+    for (uint64_t off = 0; off < n; off += batch) {
+        const uint64_t cnt = n - off < batch ? n - off : batch;
+        BinParams bp;
+        memset(&bp, 0, sizeof bp);
+        bp.f = make_params(f, keys + off, cnt, nullptr);
+        bp.recs = f->recs;
+        bp.cursor = f->cursor;
+        bp.cap = cap;
+        bp.lg_bpr = lg;
+        bp.nranges = (uint32_t)R;
+        bp.slot_out = f->slots;
+        bp.res_bits = f->resb;
+        if ((e = cudaMemsetAsync(bp.cursor, 0, R * sizeof(unsigned long long), st)) != cudaSuccess)
+            return cuda_fail(e, "binned contains: cursor reset");
+        void* args[] = {&bp};
+        const uint64_t chunks = (cnt + BIN_CHUNK - 1) / BIN_CHUNK;
+        const unsigned gb = (unsigned)(chunks < (uint64_t)waves ? chunks : waves);
+        if ((e = cudaLaunchKernel((const void*)bin_fn, dim3(gb), dim3(BIN_THREADS), args, smem, st)) != cudaSuccess)
+            return cuda_fail(e, "binned contains: bin launch");
+        if ((rc = check_launch("binned contains: bin launch"))) return rc;
+        const uint64_t tiles = (cap + 32 * LOOKUP_RPL - 1) / (32 * LOOKUP_RPL);
+        uint64_t gl = (tiles + 7) / 8;
+        if (gl > (uint64_t)waves) gl = waves;
+        for (uint32_t r = 0; r < (uint32_t)R; ++r) {  // one launch per range: the GPU stays in one L2-resident range
+            bp.range = r;
+            if ((e = cudaLaunchKernel((const void*)look_fn, dim3((unsigned)gl), dim3(256), args, 0, st)) != cudaSuccess)
+                return cuda_fail(e, "binned contains: lookup launch");
+            if ((rc = check_launch("binned contains: lookup launch"))) return rc;
+        }
+        uint32_t* o = out + off / 32;  // off is a multiple of 128
+        void* uargs[] = {&bp, &o};
+        uint64_t gu = ((cnt + 32 * UNBIN_KPL - 1) / (32 * UNBIN_KPL) + 7) / 8;
+        if (gu > (uint64_t)waves) gu = waves;
+        if ((e = cudaLaunchKernel((const void*)unbin_fn, dim3((unsigned)(gu ? gu : 1)), dim3(256), uargs, 0, st)) !=
+            cudaSuccess)
+            return cuda_fail(e, "binned contains: unbin launch");
+        if ((rc = check_launch("binned contains: unbin launch"))) return rc;
+    }
+    return BF_OK;
+}
+
+static int binned_contains(bf_filter* f, const uint64_t* keys, uint64_t n, uint32_t* out, cudaStream_t st,
+                           KernelFn bin_fn, KernelFn look_fn, KernelFn unbin_fn)
+{
+    // the scratch is shared with the binned add: same serialisation (binned_add)
+    std::lock_guard<std::mutex> g(f->mu);
+    cudaError_t e = cudaSuccess;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if ((e = cudaStreamIsCapturing(st, &cs)) != cudaSuccess) return cuda_fail(e, "binned contains: capture status");
+    const bool capturing = cs != cudaStreamCaptureStatusNone;
+    if (!f->scratch_done) {
+        if ((e = cudaEventCreateWithFlags(&f->scratch_done, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(e, "binned contains: event");
+    } else if (!capturing && (e = cudaStreamWaitEvent(st, f->scratch_done, 0)) != cudaSuccess) {
+        return cuda_fail(e, "binned contains: wait for the previous binned call");
+    }
+    int rc = binned_contains_locked(f, keys, n, out, st, bin_fn, look_fn, unbin_fn);
+    if (rc == BF_OK && !capturing && (e = cudaEventRecord(f->scratch_done, st)) != cudaSuccess)
+        return cuda_fail(e, "binned contains: event record");
+    return rc;
+}
+
 static KernelFn hybrid_kernel(const bf_filter* f)
 {
     const Sched& sc = f->sched[0];
@@ -759,7 +901,37 @@ int bf_contains(const bf_filter* f, const uint64_t* keys, uint64_t n, uint32_t* 
     if (!keys || ((uintptr_t)keys & 7)) return fail(BF_EINVAL, "keys must be a non-null 8-byte-aligned device pointer");
     if (!out_bits || ((uintptr_t)out_bits & 3)) return fail(BF_EINVAL, "out_bits must be a non-null 4-byte-aligned device pointer");
     DeviceGuard g(f->device);
+    bf_filter* mf = const_cast<bf_filter*>(f);  // scratch and path record only; the filter bits are read-only
+    KernelFn bin_fn = nullptr, look_fn = nullptr, unbin_fn = nullptr;
+    const bool want_binned =
+        f->contains_mode == BF_CONTAINS_BINNED ||
+        (f->contains_mode == BF_CONTAINS_AUTO && f->bytes >= kBinMinFilterBytes && n >= f->b);
+    if (want_binned && binned_contains_available(f, &bin_fn, &look_fn, &unbin_fn)) {
+        mf->last_contains_binned = 1;
+        return binned_contains(mf, keys, n, out_bits, (cudaStream_t)stream, bin_fn, look_fn, unbin_fn);
+    }
+    mf->last_contains_binned = 0;
     return launch_bulk(f, 1, keys, n, out_bits, (cudaStream_t)stream);
+}
+
+int bf_set_contains_mode(bf_filter* f, int mode)
+{
+    if (!f || mode < BF_CONTAINS_AUTO || mode > BF_CONTAINS_BINNED) return fail(BF_EINVAL, "bad filter or contains mode");
+    if (mode == BF_CONTAINS_BINNED) {
+        KernelFn a, b, c;
+        if (!binned_contains_available(f, &a, &b, &c))
+            return fail(BF_EUNSUPPORTED, "binned contains is not compiled for this configuration / draw scheme");
+    }
+    f->contains_mode = mode;
+    return BF_OK;
+}
+
+int bf_get_contains_mode(const bf_filter* f, int* mode, int* last_binned)
+{
+    if (!f) return fail(BF_EINVAL, "null filter");
+    if (mode) *mode = f->contains_mode;
+    if (last_binned) *last_binned = f->last_contains_binned;
+    return BF_OK;
 }
 
 // ------------------------------------------------------------ routing (NEXT N1)

@@ -43,6 +43,10 @@ struct BinParams {
     uint64_t* idx_out;           // optional: key index of every record (contains routing)
     uint64_t idx_base;           // index of keys[0]
     uint32_t blk_base;           // phase 2: first block of the local filter part
+    // binned contains: the record slot of every key of the batch (key order;
+    // 0xFFFFFFFF = its bucket was full) and one result bit per record slot
+    uint32_t* slot_out;
+    uint32_t* res_bits;
 };
 
 // 512 threads x 8 keys: 177-180 Gkeys/s for the bin phase at R = 256 vs 162-166
@@ -292,13 +296,13 @@ __host__ __device__ inline size_t bin_range_smem_bytes(uint32_t nranges, uint32_
     return (size_t)chunk * 8 + rp * 4 * 3 + 16;
 }
 
-template <class C1, int NT, int KPT, bool FULL>
+template <class C1, int NT, int KPT, bool FULL, bool SLOTS>
 __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, uint32_t cnt, uint32_t R,
                                                 uint32_t chunk_no, uint64_t* stage, uint32_t* cnt2, uint32_t* rbase,
                                                 uint32_t* flags, uint32_t* warp_tot, const SaltSrc<C1>& ss,
                                                 uint64_t* const recs, unsigned long long* const cursor,
                                                 const uint32_t cap, const uint64_t seed, const uint32_t b32,
-                                                const uint32_t lg_bpr, const uint64_t pol)
+                                                const uint32_t lg_bpr, const uint64_t pol, uint32_t* const slot_out)
 {
     using W = typename C1::W;
     constexpr int CHUNK = NT * KPT;
@@ -410,10 +414,37 @@ __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, 
         }
     }
     __syncthreads();
-    // (c) sorted slots in shared memory
+    // (c) sorted slots in shared memory (binned contains: and every key's
+    // record slot, rbase[r] + its sorted position, in key order)
+    uint32_t* const so = SLOTS ? slot_out + base + (uint64_t)tid * KPT : nullptr;
 #pragma unroll
-    for (int i = 0; i < KPT; ++i) {
-        if (FULL || tid * KPT + i < cnt) stage[hist[rl[i] >> 16] + (rl[i] & 0xFFFFu)] = rec[i];
+    for (int i0 = 0; i0 < KPT; i0 += 4) {  // slots leave 4 at a time (16-byte stores, few live registers)
+        uint32_t sl[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int i = i0 + c;
+            sl[c] = 0xFFFFFFFFu;
+            if (FULL || tid * KPT + i < cnt) {
+                const uint32_t r = rl[i] >> 16;
+                const uint32_t pos = hist[r] + (rl[i] & 0xFFFFu);
+                stage[pos] = rec[i];
+                if constexpr (SLOTS) {
+                    const uint32_t d = rbase[r] + pos;
+                    sl[c] = d - r * cap < cap ? d : 0xFFFFFFFFu;  // a full bucket: the key is looked up directly
+                }
+            }
+        }
+        if constexpr (SLOTS) {
+            if (FULL) {
+                asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(so + i0), "r"(sl[0]), "r"(sl[1]),
+                             "r"(sl[2]), "r"(sl[3])
+                             : "memory");
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (tid * KPT + i0 + c < cnt) so[i0 + c] = sl[c];
+            }
+        }
     }
     if (tid == 0) flags[(chunk_no & 1u) ^ 1u] = 0u;  // the next chunk's overflow flag
     __syncthreads();
@@ -436,13 +467,13 @@ __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, 
                 const uint32_t r = (uint32_t)(v >> 32) >> lg_bpr;
                 const uint32_t d = rbase[r] + j;
                 if (d - r * cap < cap) st_evict_first(recs + d, v, pol);
-                else add_part<C1>((W*)p.words, (uint32_t)v, (uint32_t)(v >> 32), 0, ss);
+                else if constexpr (!SLOTS) add_part<C1>((W*)p.words, (uint32_t)v, (uint32_t)(v >> 32), 0, ss);
             }
         }
     }
 }
 
-template <class C1, int NT = BIN_THREADS, int KPT = BIN_KPT, int MINB = BIN_RANGE_MINB>
+template <class C1, int NT = BIN_THREADS, int KPT = BIN_KPT, int MINB = BIN_RANGE_MINB, bool SLOTS = false>
 __global__ void __launch_bounds__(NT, MINB) bin_range_kernel(const BinParams bp)
 {
     constexpr int CHUNK = NT * KPT;
@@ -479,11 +510,12 @@ __global__ void __launch_bounds__(NT, MINB) bin_range_kernel(const BinParams bp)
             }
         }
         if (cnt == CHUNK && vec_ok)
-            bin_range_chunk<C1, NT, KPT, true>(p, base, cnt, R, chunk_no, stage, cnt2, rbase, flags, warp_tot, ss,
-                                               recs, cursor, cap, seed, b32, lg_bpr, pol);
+            bin_range_chunk<C1, NT, KPT, true, SLOTS>(p, base, cnt, R, chunk_no, stage, cnt2, rbase, flags, warp_tot,
+                                                      ss, recs, cursor, cap, seed, b32, lg_bpr, pol, bp.slot_out);
         else
-            bin_range_chunk<C1, NT, KPT, false>(p, base, cnt, R, chunk_no, stage, cnt2, rbase, flags, warp_tot, ss,
-                                                recs, cursor, cap, seed, b32, lg_bpr, pol);
+            bin_range_chunk<C1, NT, KPT, false, SLOTS>(p, base, cnt, R, chunk_no, stage, cnt2, rbase, flags,
+                                                       warp_tot, ss, recs, cursor, cap, seed, b32, lg_bpr, pol,
+                                                       bp.slot_out);
     }
 }
 
@@ -618,6 +650,124 @@ __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
                 }
             }
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Binned contains (round 2b) for filters much larger than L2, the lookup
+// counterpart of the binned add: bin_range_kernel<..., SLOTS> bins the
+// queries by filter range and writes each key's record slot; lookup_kernel
+// then tests the records of ONE range (L2-resident while the whole GPU works
+// in it; one launch per range) and writes one result bit per record slot,
+// packed by ballot; unbin_kernel gathers every key's bit through its slot
+// back into key order.  The answers are exactly those of the direct kernel
+// (same block, same pattern; tests/test_gpu_parity.py).  A key whose bucket
+// was full (slot 0xFFFFFFFF; never with uniform hashes) is looked up
+// directly by unbin_kernel.  C is the Θ = 1, Φ = s contains configuration.
+constexpr int LOOKUP_RPL = 4;  // records per lane per tile (loads in flight)
+
+template <class C>
+__global__ void __launch_bounds__(256) lookup_kernel(const BinParams bp)
+{
+    using W = typename C::W;
+    constexpr int RK = LOOKUP_RPL;
+    constexpr uint64_t TILE = 32 * RK;
+    SaltSrc<C> ss;
+    ss.init(0, nullptr, nullptr);
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const W* F = (const W*)bp.f.words;
+    const uint64_t r = bp.range;
+    const uint64_t cnt = min((uint64_t)bp.cursor[r], bp.cap);
+    const uint64_t ntile = (cnt + TILE - 1) / TILE;
+    const uint64_t* rb = bp.recs + r * bp.cap;
+    uint32_t* res = bp.res_bits + (r * bp.cap) / 32;  // cap is a multiple of 128
+    // (a software prefetch of the next tile's records measured slower: 74
+    // registers, 11.0 -> 11.8 ms per 2^31 records; so did 2 and 8 records per lane)
+    for (uint64_t lt = gw; lt < ntile; lt += nw) {
+        const uint64_t s0 = lt * TILE;
+        uint64_t v[RK];
+        bool ok[RK];
+#pragma unroll
+        for (int j = 0; j < RK; ++j) {  // slot s0 + 32 j + lane: 256 contiguous bytes per warp load
+            ok[j] = s0 + 32 * j + lane < cnt;
+            v[j] = ok[j] ? ld_key1(rb + s0 + 32 * j + lane) : 0ULL;
+        }
+        W wd[RK][C::s];
+#pragma unroll
+        for (int j = 0; j < RK; ++j)
+            if (ok[j]) load_block<C>(F, (uint32_t)(v[j] >> 32) - bp.blk_base, wd[j]);
+        uint32_t mine = 0;
+#pragma unroll
+        for (int j = 0; j < RK; ++j) {
+            const bool hit = ok[j] && test_block<C>(wd[j], Draws<C>((uint32_t)v[j]), ss);
+            const uint32_t ball = __ballot_sync(0xffffffffu, hit);
+            if (lane == (uint32_t)j) mine = ball;
+        }
+        if (lane < (uint32_t)RK) res[s0 / 32 + lane] = mine;
+    }
+}
+
+// Key order again: bit i of the batch's result words = the result bit of
+// key i's record slot.  out points at the batch's first result word.  A lane
+// takes 8 consecutive keys (two 16-byte slot loads, the next tile's slots
+// loaded while this tile's bits are gathered), and the result words leave
+// packed as in the bulk kernel (store_results).
+constexpr int UNBIN_KPL = 8;
+
+template <class C>
+__global__ void __launch_bounds__(256) unbin_kernel(const BinParams bp, uint32_t* out)
+{
+    using W = typename C::W;
+    constexpr int UK = UNBIN_KPL;
+    constexpr uint64_t TILE = 32 * UK;
+    SaltSrc<C> ss;
+    ss.init(0, nullptr, nullptr);
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t n = bp.f.n;
+    const uint64_t ntile = (n + TILE - 1) / TILE;
+    const uint64_t nwords = (n + 31) / 32;
+    const uint32_t* res = bp.res_bits;
+    auto load = [&](uint64_t lt, uint32_t (&sl)[UK]) {
+        const uint64_t i0 = lt * TILE + (uint64_t)lane * UK;
+        if (i0 + UK <= n) {  // slot_out is 256-byte aligned and i0 a multiple of 8
+#pragma unroll
+            for (int c = 0; c < UK; c += 4)
+                asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                    : "=r"(sl[c]), "=r"(sl[c + 1]), "=r"(sl[c + 2]), "=r"(sl[c + 3])
+                    : "l"(bp.slot_out + i0 + c));
+        } else {
+#pragma unroll
+            for (int c = 0; c < UK; ++c) sl[c] = i0 + c < n ? bp.slot_out[i0 + c] : 0xFFFFFFFEu;  // FE: past the end
+        }
+    };
+    uint32_t cur[UK], nxt[UK];
+    if (gw < ntile) load(gw, cur);
+    for (uint64_t lt = gw; lt < ntile; lt += nw) {
+        if (lt + nw < ntile) load(lt + nw, nxt);
+        uint32_t w[UK];
+#pragma unroll
+        for (int c = 0; c < UK; ++c) w[c] = cur[c] < 0xFFFFFFFEu ? __ldg(res + (cur[c] >> 5)) : 0u;
+        uint32_t bits = 0;
+#pragma unroll
+        for (int c = 0; c < UK; ++c) {
+            uint32_t hit = (w[c] >> (cur[c] & 31u)) & 1u;
+            if (cur[c] >= 0xFFFFFFFEu) hit = 0;
+            if (cur[c] == 0xFFFFFFFFu) {  // the key's bucket was full: look it up directly
+                const uint64_t key = bp.f.keys[lt * TILE + (uint64_t)lane * UK + c];
+                const uint64_t h = xxh64_u64(key, bp.f.seed);
+                W wd[C::s];
+                load_block<C>((const W*)bp.f.words, block_of(h, bp.f.b32), wd);
+                hit = test_block<C>(wd, Draws<C>((uint32_t)h), ss);
+            }
+            bits |= hit << c;
+        }
+        store_results<UK>(out, lt, bits, lane, nwords);
+#pragma unroll
+        for (int c = 0; c < UK; ++c) cur[c] = nxt[c];
     }
 }
 

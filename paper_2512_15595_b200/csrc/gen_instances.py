@@ -184,6 +184,9 @@ def emit():
             binned.append((6, v, B, S, k, z, 1, 1, 1, 0))  # bin by owner (routing, NEXT N1)
             binned.append((3, v, B, S, k, z, theta, phi, kpt, hv))
             binned.append((4, v, B, S, k, z, 1, B // S, 1, 0))  # routed contains (Θ=1, Φ=s)
+            binned.append((7, v, B, S, k, z, 1, 1, 1, 0))  # bin by range + key slots (binned contains)
+            binned.append((8, v, B, S, k, z, 1, B // S, 1, 0))  # binned contains: per-range lookup
+            binned.append((9, v, B, S, k, z, 1, B // S, 1, 0))  # binned contains: back to key order
             if (v, B, S, k, z) in HYBRID:
                 binned.append((5, v, B, S, k, z, theta, phi, kpt, hv))  # hybrid TMA+LSU add (N4 experiment)
     inst = inst + binned + scheme_instances()
@@ -201,6 +204,12 @@ def emit():
                 fn = f"bin_kernel<{cfg_type(i)}, true>"
             elif op == 3:
                 fn = f"apply_kernel<{cfg_type(i)}>"
+            elif op == 7:
+                fn = f"bin_range_kernel<{cfg_type(i)}, BIN_THREADS, BIN_KPT, BIN_RANGE_MINB, true>"
+            elif op == 8:
+                fn = f"lookup_kernel<{cfg_type(i)}>"
+            elif op == 9:
+                fn = f"unbin_kernel<{cfg_type(i)}>"
             elif op == 4:
                 fn = f"contains_bucket_kernel<{cfg_type(i)}>"
             elif op == 5:

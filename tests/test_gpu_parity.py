@@ -401,6 +401,86 @@ def test_binned_add_bucket_overflow(bflib, cuda):
     assert np.array_equal(_gpu_bytes(f), o.bytes())
 
 
+@pytest.mark.parametrize("cfg", BINNED_CFGS)
+@pytest.mark.parametrize("range_bytes,batch,misalign", [(1 << 16, 0, 0), (1 << 15, 30_000, 0), (3 << 14, 7_777, 0),
+                                                         (1 << 10, 0, 0), (1 << 16, 0, 1)])
+def test_binned_contains_matches_oracle(bflib, cuda, cfg, range_bytes, batch, misalign):
+    """BF_CONTAINS_BINNED (bin the queries by filter range with their record
+    slots, test range by range, gather back to key order) answers exactly as
+    the oracle: several ranges, batches that are not multiples of 128 (cut
+    to whole result words), a ragged last range and result word, R > 512
+    buckets, keys off a 32-byte boundary."""
+    import torch
+    bf = bflib
+    v, B, S, k, z = cfg
+    m = (1 << 22) + 5 * B
+    keys = synth.keys(321, 100_003)
+    o = OracleFilter(v, m, B=B, S=S, k=k, z=z)
+    o.add(keys)
+    f = bf.Filter(m, k, B, S, variant=v, z=z)
+    f.add(_to_dev(torch, keys, cuda))
+    f.set_add_mode(bf.BF_ADD_AUTO, range_bytes, batch)
+    f.set_contains_mode(bf.BF_CONTAINS_BINNED)
+    q = np.concatenate([keys[:60_001], synth.negatives(60_013)])
+    if misalign:
+        qd = torch.empty(q.size + 1, dtype=torch.int64, device=cuda)
+        qd[1:].copy_(_to_dev(torch, q, cuda))
+        qd = qd[1:]
+    else:
+        qd = _to_dev(torch, q, cuda)
+    got = _gpu_contains(torch, f, qd)
+    assert f.contains_mode() == (bf.BF_CONTAINS_BINNED, 1)
+    assert np.array_equal(got, o.contains(q))
+
+
+def test_binned_contains_bucket_overflow(bflib, cuda):
+    """Queries concentrated in one range overflow its bucket; those keys are
+    looked up directly (slot marker) and every answer is still exact."""
+    import torch
+    bf = bflib
+    m, B = 1 << 22, 256
+    o_geom = OracleFilter(3, m, B=B, S=64, k=8, allocate=False)
+    cand = synth.keys(9, 200_000)
+    per_range = (1 << 15) // (B // 8)
+    hot = np.array([key for key in cand if o_geom.pattern(int(key))[0] < per_range], dtype=np.uint64)
+    keys = cand[:50_000]
+    o = OracleFilter(3, m, B=B, S=64, k=8)
+    o.add(keys)
+    f = bf.Filter(m, 8, B, 64, "SBF")
+    f.add(_to_dev(torch, keys, cuda))
+    f.set_add_mode(bf.BF_ADD_AUTO, 1 << 15, 0)
+    f.set_contains_mode(bf.BF_CONTAINS_BINNED)
+    q = np.concatenate([hot, hot, keys[:20_000], synth.negatives(7)])
+    assert hot.size > 4000
+    got = _gpu_contains(torch, f, _to_dev(torch, q, cuda))
+    assert f.contains_mode()[1] == 1
+    assert np.array_equal(got, o.contains(q))
+
+
+def test_binned_contains_auto_policy(bflib, cuda):
+    """AUTO takes the binned lookup only for a filter >= 96 MiB queried with at
+    least one key per block; answers equal the direct path's."""
+    import torch
+    bf = bflib
+    m = 1 << 30  # 128 MiB, b = 2^22 blocks of 256 bits
+    f = bf.Filter(m, 8, 256, 64, "SBF")
+    kd = torch.empty(1 << 22, dtype=torch.int64, device=cuda)
+    bf.bf_keygen(kd, kd.numel(), 5)
+    f.add(kd)
+    qd = torch.empty((1 << 22) + 77, dtype=torch.int64, device=cuda)
+    bf.bf_keygen(qd, qd.numel(), 3)  # half overlap with the added keys
+    small = f.contains(qd[:1024])
+    assert f.contains_mode() == (bf.BF_CONTAINS_AUTO, 0)
+    big = f.contains(qd)
+    assert f.contains_mode() == (bf.BF_CONTAINS_AUTO, 1)
+    f.set_contains_mode(bf.BF_CONTAINS_DIRECT)
+    ref = f.contains(qd)
+    assert f.contains_mode() == (bf.BF_CONTAINS_DIRECT, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(big, ref) and torch.equal(small, ref[:32])
+    assert int((ref == 0).sum()) < ref.numel()
+
+
 def test_binned_add_large_filter_sampled(bflib, cuda):
     """Binned add on an 8 GiB filter (256 ranges of 32 MiB): sampled block
     ranges equal the oracle's."""
