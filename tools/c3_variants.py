@@ -93,9 +93,20 @@ def main():
         f.set_add_mode(bf.BF_ADD_AUTO)
         add()
         t_con = timed(lambda: f.contains(keys, out))
+        con_binned = f.contains_mode()[1]
         fn_ok = int((out != -1).sum().item()) == 0
         t_neg = timed(lambda: f.contains(neg, outn))
+        neg_binned = f.contains_mode()[1]
         fp = int(lut[outn.view(torch.uint8).long()].sum().item())
+        outn_auto = outn.clone()
+        f.set_contains_mode(bf.BF_CONTAINS_DIRECT)  # the direct lookup for comparison: same answers
+        t_con_direct = timed(lambda: f.contains(keys, out), 1)
+        fn_ok = fn_ok and int((out != -1).sum().item()) == 0
+        f.contains(neg, outn)
+        torch.cuda.synchronize()
+        same_neg = bool(torch.equal(outn, outn_auto))
+        f.set_contains_mode(bf.BF_CONTAINS_AUTO)
+        del outn_auto
         p = row["fpr_model"]
         zz = (fp - q * p) / math.sqrt(q * p * (1 - p))
         # parity on a sampled range (middle of the filter, 2^14 blocks), checked after the loop
@@ -109,6 +120,10 @@ def main():
                "add_gkeys_s": round(n / t_add / 1e6, 3), "add_path": "binned" if binned else "direct",
                "add_direct_gkeys_s": round(n / t_direct / 1e6, 3),
                "contains_gkeys_s": round(n / t_con / 1e6, 3), "contains_neg_gkeys_s": round(q / t_neg / 1e6, 3),
+               "contains_path": "binned" if con_binned else "direct",
+               "contains_neg_path": "binned" if neg_binned else "direct",
+               "contains_direct_gkeys_s": round(n / t_con_direct / 1e6, 3),
+               "negatives_same_answers_both_paths": same_neg,
                "step_gkeys_s": round(2 * n / (t_add + t_con) / 1e6, 3),
                "fpr_measured": fp / q, "fpr_model": p, "fpr_z": round(zz, 2), "negatives": q,
                "no_false_negatives": fn_ok, "parity_sampled_range": [lo, hi], "parity": par,
@@ -128,18 +143,22 @@ def main():
             fh.write(json.dumps(r) + "\n")
     with open(out_prefix + ".md", "w") as fh:
         fh.write("# configs[2]: five filter variants at 8 GiB (HBM-resident), 2^32 keys, one B200\n\n"
-                 "`tools/c3_variants.py`. Gkeys/s, CUDA-event median. add = library default (binned), "
-                 "direct = bf_add with BF_ADD_DIRECT. FPR on 2^28 negatives vs the exact model; parity: "
+                 "`tools/c3_variants.py`. Gkeys/s, CUDA-event median. add / contains = library default "
+                 "(AUTO: binned add; binned contains when the call has >= one key per block, path in brackets), "
+                 "direct = BF_ADD_DIRECT / BF_CONTAINS_DIRECT. FPR on 2^28 negatives vs the exact model; "
+                 "same = the 2^28 negatives answer identically through both contains paths; parity: "
                  "a 2^14-block range in the middle of the filter equals the range-restricted oracle's "
                  "(all 2^32 keys hashed on the host).\n\n")
-        fh.write("| variant | B/S | k | z | add (binned) | add (direct) | contains pos | contains neg | "
-                 "add+contains | FPR measured | FPR model | z | FN | parity |\n"
-                 "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
+        fh.write("| variant | B/S | k | z | add (binned) | add (direct) | contains pos | contains pos (direct) | "
+                 "contains neg | add+contains | FPR measured | FPR model | z | FN | same | parity |\n"
+                 "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
         for r in rows:
             fh.write(f"| {r['variant']} | {r['B']}/{r['S']} | {r['k']} | {r['z']} | {r['add_gkeys_s']} | "
-                     f"{r['add_direct_gkeys_s']} | {r['contains_gkeys_s']} | {r['contains_neg_gkeys_s']} | "
+                     f"{r['add_direct_gkeys_s']} | {r['contains_gkeys_s']} ({r['contains_path']}) | "
+                     f"{r['contains_direct_gkeys_s']} | {r['contains_neg_gkeys_s']} ({r['contains_neg_path']}) | "
                      f"{r['step_gkeys_s']} | {r['fpr_measured']:.3e} | {r['fpr_model']:.3e} | {r['fpr_z']:+.1f} | "
-                     f"{'none' if r['no_false_negatives'] else 'FOUND'} | {r['parity']} |\n")
+                     f"{'none' if r['no_false_negatives'] else 'FOUND'} | "
+                     f"{'yes' if r['negatives_same_answers_both_paths'] else 'NO'} | {r['parity']} |\n")
 
 
 if __name__ == "__main__":

@@ -27,13 +27,14 @@ def render(path, title):
         if r["kpt"] == 1:
             hv[(r["k"], r["op"], r["theta"], r["phi"], r["hv"])] = r["gkeys_s"]
     thetas = sorted({r["theta"] for r in rows})
-    binned = {r["k"]: r["gkeys_s"] for r in rows if r["op"] == "add_binned"}
-    print("Every add column is the direct add (like for like); the binned add (default schedule) is its own column.\n")
-    print("| k | op | " + " | ".join(f"Θ={t}" for t in thetas) + " | binned add |")
+    binned = {(r["k"], r["op"][:-len("_binned")]): r["gkeys_s"] for r in rows if r["op"].endswith("_binned")}
+    print("Every Θ column is the direct kernel (like for like); the binned add / contains (round 2b; default "
+          "schedule) are their own column.\n")
+    print("| k | op | " + " | ".join(f"Θ={t}" for t in thetas) + " | binned |")
     print("|---|---|" + "---|" * len(thetas) + "---|")
     for k in sorted({r["k"] for r in rows}):
         for op in ("contains", "add"):
-            extra = f"{binned[k]:.2f}" if op == "add" and k in binned else "—"
+            extra = f"{binned[(k, op)]:.2f}" if (k, op) in binned else "—"
             print(f"| {k} | {op} | " + " | ".join(f"{best.get((k, op, t), 0):.2f}" for t in thetas) + f" | {extra} |")
     print("\nHash variants at KPT=1 (H0 immediates/registers, H1 constant table, H2 smem table, H3 per-lane re-hash):\n")
     print("| k | op | layout | H0 | H1 | H2 | H3 |\n|---|---|---|---|---|---|---|")

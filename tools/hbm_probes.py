@@ -62,6 +62,7 @@ def main():
     if not a.no_product:
         f = bf.Filter(nbytes * 8, 8, 256, 64, "SBF")
         f.set_add_mode(bf.BF_ADD_DIRECT)
+        f.set_contains_mode(bf.BF_CONTAINS_DIRECT)
         f.add(keys)
     base = bf.bf_get_l2_fetch_granularity()
     if a.sweep2:

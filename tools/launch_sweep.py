@@ -43,6 +43,7 @@ def main():
     for v, B, S, k, z in cfgs:
         f = bf.Filter(a.m_bits, k, B, S, v, z=z)
         f.set_add_mode(bf.BF_ADD_DIRECT)
+        f.set_contains_mode(bf.BF_CONTAINS_DIRECT)
         f.add(keys)
         for op in (1, 0):
             occ = bf.bf_get_launch(f.handle, op)[1]

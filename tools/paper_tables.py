@@ -27,14 +27,15 @@ def main(paper, ablation=None):
     print(f"# The paper's Table 1 / Table 2 grid on this B200 (`{os.path.basename(paper)}`)\n")
     print("SBF, S=64, k=16 (B=64 is the RBBF), 2^28 keys, every Θ with Φ = s/Θ, best KPT of 1/2/4,")
     print("CUDA-event median of 3 launches. Cells: **ours** (paper, P:L326-336 / P:L371-381), G keys/s.")
-    print("add = the paper's method (direct red.global.or); `add_binned` = our binned add (bf_binned.cuh).\n")
+    print("add / contains = the paper's method (direct red.global.or / block loads); `add_binned`, "
+          "`contains_binned` = our binned add and binned contains (bf_binned.cuh).\n")
     thetas = (1, 2, 4, 8, 16)
     for size, title in (("32MB", "Table 2: 32 MiB (L2-resident) filter"), ("1GB", "Table 1: 1 GiB (HBM-resident) filter")):
         print(f"## {title}\n")
         print("| op | B | " + " | ".join(f"Θ={t}" for t in thetas) + " |")
         print("|---|---|" + "---|" * len(thetas))
         wins = total = 0
-        for op in ("contains", "add", "add_binned"):
+        for op in ("contains", "add", "add_binned", "contains_binned"):
             for B in (64, 128, 256, 512, 1024):
                 cells = []
                 any_cell = False

@@ -99,9 +99,10 @@ def main():
         v, B, S, k, z = cfg
         m = m_of(cfg)
         f = bf.Filter(m, k, B, S, v, z=z)
-        # like-for-like Θ sweep: the direct add for every schedule (the
-        # binned add is one separate row below, default schedule)
+        # like-for-like Θ sweep: the direct add and contains for every
+        # schedule (the binned add / contains are separate rows below)
         f.set_add_mode(bf.BF_ADD_DIRECT)
+        f.set_contains_mode(bf.BF_CONTAINS_DIRECT)
         for op, th, ph, kpt, hv in sorted(scheds):
             f.set_layout(op, th, ph, kpt, hv)
             ts = []
@@ -152,6 +153,23 @@ def main():
             if fh:
                 fh.write(json.dumps(rec) + "\n")
             f.set_add_mode(bf.BF_ADD_DIRECT)
+            f.set_contains_mode(bf.BF_CONTAINS_BINNED)  # the binned contains, as its own row
+            ts = []
+            for r in range(a.reps + 1):
+                e0.record(st)
+                f.contains(keys, out)
+                e1.record(st)
+                torch.cuda.synchronize()
+                if r:
+                    ts.append(e0.elapsed_time(e1))
+            t = statistics.median(ts)
+            rec = {"set": a.set, "variant": v, "B": B, "S": S, "k": k, "z": z, "m_bits": m, "n": n,
+                   "op": "contains_binned", "theta": 1, "phi": B // S, "kpt": 4, "hv": 0,
+                   "ms": round(t, 4), "gkeys_s": round(n / (t * 1e-3) / 1e9, 3)}
+            print(json.dumps(rec), flush=True)
+            if fh:
+                fh.write(json.dumps(rec) + "\n")
+            f.set_contains_mode(bf.BF_CONTAINS_DIRECT)
         f.clear()
         f.add(keys)
         f.contains(keys, out)
@@ -254,6 +272,7 @@ def paper_tables(a, torch, bf, dev):
             s = B // 64
             v = 2 if B == 64 else 3
             f = bf.Filter(m, 16, B, 64, v)
+            f.set_contains_mode(bf.BF_CONTAINS_DIRECT)  # the paper's direct lookup for every Θ
             for op in ("add", "contains"):
                 for ti, th in enumerate([1 << i for i in range(s.bit_length())]):
                     best = None
@@ -288,6 +307,13 @@ def paper_tables(a, torch, bf, dev):
                 rec = {"set": "paper", "size": size, "m_bits": m, "B": B, "S": 64, "k": 16, "op": "add_binned",
                        "theta": f.layout(0)["theta"], "phi": f.layout(0)["phi"], "kpt": f.layout(0)["kpt"],
                        "gkeys_s": round(n / (t * 1e-3) / 1e9, 2), "n": n}
+                print(json.dumps(rec), flush=True)
+                if fh:
+                    fh.write(json.dumps(rec) + "\n")
+                f.set_contains_mode(bf.BF_CONTAINS_BINNED)
+                t = timeit(lambda: f.contains(keys, out), a.reps)
+                rec = {"set": "paper", "size": size, "m_bits": m, "B": B, "S": 64, "k": 16, "op": "contains_binned",
+                       "theta": 1, "phi": s, "kpt": 4, "gkeys_s": round(n / (t * 1e-3) / 1e9, 2), "n": n}
                 print(json.dumps(rec), flush=True)
                 if fh:
                     fh.write(json.dumps(rec) + "\n")
@@ -348,6 +374,7 @@ def hash_ablation(a, torch, bf, dev):
         for scheme, name in ((2, "sbf_iterative"), (1, "sbf_double"), (0, "sbf_multiplicative")):
             f = bf.Filter(m, 16, 256, 64, "SBF", scheme=scheme)
             f.set_add_mode(bf.BF_ADD_DIRECT)
+            f.set_contains_mode(bf.BF_CONTAINS_DIRECT)  # the paper's lookup at every step
             for lay_name, add_lay, con_lay in (("theta1_kpt1", (1, 4, 1), (1, 4, 1)),
                                                ("optimised", (4, 1, 4) if scheme != 2 else (1, 4, 1),
                                                 (1, 4, 4) if scheme != 2 else (1, 4, 1))):
