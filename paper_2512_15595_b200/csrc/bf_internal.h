@@ -11,16 +11,20 @@ typedef void (*KernelFn)(Params);
 
 // Key of a specialized kernel instantiation.
 struct InstKey {
-    uint8_t op;       // 0 add, 1 contains, 2 bin by range, 3 apply bucket, 4 contains bucket, 5 hybrid add, 6 bin by owner
+    uint8_t op;       // 0 add, 1 contains, 2 bin by range, 3 apply bucket, 4 contains bucket, 5 hybrid add,
+                      // 6 bin by owner, 7 bin by range + key slots, 8 range lookup, 9 unbin (binned contains)
     uint8_t variant;  // BF_BBF..BF_CSBF
     uint16_t B;
     uint8_t S, k, z, theta, phi, kpt, hv;
     uint8_t hs = 0;   // draw scheme (0 multiplicative, 1 double hashing, 2 iterative)
+    // disjoint bit fields: op 4 bits (< 16), variant 3, B/32 6 (B <= 1024 -> <= 32), S 1, k 6 (<= 32),
+    // z 6, theta 6, phi 6, kpt 4, hv 4, hs 2
     uint64_t pack() const
     {
-        return (uint64_t)op | ((uint64_t)variant << 3) | ((uint64_t)(B / 32) << 6) | ((uint64_t)(S == 64) << 12) |
-               ((uint64_t)k << 13) | ((uint64_t)z << 19) | ((uint64_t)theta << 25) | ((uint64_t)phi << 31) |
-               ((uint64_t)kpt << 37) | ((uint64_t)hv << 41) | ((uint64_t)hs << 45);
+        return (uint64_t)(op & 15) | ((uint64_t)(variant & 7) << 4) | ((uint64_t)(B / 32) << 7) |
+               ((uint64_t)(S == 64) << 13) | ((uint64_t)k << 14) | ((uint64_t)z << 20) | ((uint64_t)theta << 26) |
+               ((uint64_t)phi << 32) | ((uint64_t)(kpt & 15) << 38) | ((uint64_t)(hv & 15) << 42) |
+               ((uint64_t)(hs & 3) << 46);
     }
 };
 
