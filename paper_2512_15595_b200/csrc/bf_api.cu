@@ -225,13 +225,11 @@ static int pick_grid(bf_filter* f, KernelFn fn) { return occupancy(fn) * sm_coun
 // launch, and the random request stream it produces reaches the L2/HBM in
 // bursts; retiring and starting CTAs de-synchronises it.
 static const int kWaveCtasPerSm = 32;
-static int range_cps()  // EXPERIMENT (temporary): CTAs per SM of the per-range apply / lookup launches
-{
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("BF_EXP_RANGE_CPS");
-        v = e ? atoi(e) : kWaveCtasPerSm;
-    }
+// CTAs per SM of the binned contains' per-range lookup launches (one launch
+// per L2-resident range, ~8M records each): 8 -- 82.2 vs 80.8 Gkeys/s at 32
+// (configs[2], 2^31 keys; tools/binned_contains_prof.py).  The binned add's
+// apply launches keep the waves of 32 (72.2 vs 68.1 at 4).
+static const int kLookupCtasPerSm = 8;
     return v;
 }
 static int g_probe_ctas_per_sm = kWaveCtasPerSm;
@@ -660,7 +658,7 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
     cudaFuncSetAttribute((const void*)bin_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // waves of CTAs like the bulk kernels (bin phase 178 -> 180 Gkeys/s vs the occupancy grid, tools/kexp bin2)
     const int grid_bin = kWaveCtasPerSm * sm_count(f->device);
-    const int grid_apply = range_cps() * sm_count(f->device);
+    const int grid_apply = kWaveCtasPerSm * sm_count(f->device);
     cudaStream_t side = tuning::BINNED_OVERLAP ? f->side : st;
     uint64_t i = 0;
     for (uint64_t off = 0; off < n; off += batch, ++i) {
@@ -800,7 +798,7 @@ static int binned_contains_locked(bf_filter* f, const uint64_t* keys, uint64_t n
         if ((rc = check_launch("binned contains: bin launch"))) return rc;
         const uint64_t tiles = (cap + 32 * LOOKUP_RPL - 1) / (32 * LOOKUP_RPL);
         uint64_t gl = (tiles + 7) / 8;
-        if (gl > (uint64_t)range_cps() * sm_count(f->device)) gl = (uint64_t)range_cps() * sm_count(f->device);
+        if (gl > (uint64_t)kLookupCtasPerSm * sm_count(f->device)) gl = (uint64_t)kLookupCtasPerSm * sm_count(f->device);
         for (uint32_t r = 0; r < (uint32_t)R; ++r) {  // one launch per range: the GPU stays in one L2-resident range
             bp.range = r;
             if ((e = cudaLaunchKernel((const void*)look_fn, dim3((unsigned)gl), dim3(256), args, 0, st)) != cudaSuccess)
