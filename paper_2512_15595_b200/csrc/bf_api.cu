@@ -230,8 +230,6 @@ static const int kWaveCtasPerSm = 32;
 // (configs[2], 2^31 keys; tools/binned_contains_prof.py).  The binned add's
 // apply launches keep the waves of 32 (72.2 vs 68.1 at 4).
 static const int kLookupCtasPerSm = 8;
-    return v;
-}
 static int g_probe_ctas_per_sm = kWaveCtasPerSm;
 
 static int set_sched(bf_filter* f, int op, int theta, int phi, int kpt, int hv)
