@@ -7,6 +7,7 @@
 #   prof      ncu --set full of the bench's bulk kernels (extra args go to bench.py)
 #   sanitize  compute-sanitizer memcheck / racecheck / synccheck over tools/sanitize_run.py
 #   profbin   ncu --set full of the binned add's bin + apply kernels (configs[2], one 2^31-key batch)
+#   profbc    ncu --set full of the binned contains' kernels (bin with slots, range lookup, unbin)
 # Everything lands in gpurun_out/ with the TAG in its name.
 set -u
 JOB=${1:-suite}
@@ -40,6 +41,13 @@ profbin)
     -o gpurun_out/profbin_$TAG python bench.py --config c3 --steps 1 --warmup 0 --no-e2e --no-cpu --no-probe --no-graph "$@" \
     > gpurun_out/profbin_$TAG.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/profbin_$TAG.log
+  ;;
+profbc)
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"lookup_kernel|unbin_kernel" -c 2 \
+    -o gpurun_out/profbc_$TAG python tools/binned_contains_prof.py > gpurun_out/profbc_$TAG.log 2>&1
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:bin_range_kernel -s 4 -c 1 \
+    -o gpurun_out/profbcbin_$TAG python tools/binned_contains_prof.py >> gpurun_out/profbc_$TAG.log 2>&1
+  echo "ncu rc=$?" >> gpurun_out/profbc_$TAG.log
   ;;
 sanitize)
   for tool in memcheck racecheck synccheck; do
