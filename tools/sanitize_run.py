@@ -34,13 +34,16 @@ for v, B, S, k, z, mode in [(3, 256, 64, 8, 0, bf.BF_ADD_DIRECT), (3, 256, 64, 8
     o.add(keys, threads=os.cpu_count())
     f = bf.Filter(m, k, B if v else 256, S if v else 64, v, z=z)
     f.set_add_mode(mode, 1 << 20, 1 << 20)  # binned: 8 ranges x 5 batches
+    if mode == bf.BF_ADD_BINNED:  # and the binned contains (same ranges and batches)
+        f.set_contains_mode(bf.BF_CONTAINS_BINNED)
     f.add(kd)
     out = f.contains(qd)
     torch.cuda.synchronize()
     got = f.data().cpu().numpy()
     good = np.array_equal(got[:o.nbytes], o.bytes()) and \
         np.array_equal(out.cpu().numpy().view(np.uint32), o.contains(q, threads=os.cpu_count()))
-    print(f"variant={v} B={B} S={S} k={k} z={z} mode={mode}: {'ok' if good else 'MISMATCH'}", flush=True)
+    print(f"variant={v} B={B} S={S} k={k} z={z} mode={mode} contains_binned={f.contains_mode()[1] if v else 0}: "
+          f"{'ok' if good else 'MISMATCH'}", flush=True)
     ok &= good
 # routing + scatter
 P = 3
