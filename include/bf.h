@@ -199,8 +199,8 @@ int bf_get_add_mode(const bf_filter* f, int* mode, int* last_binned);
  *                       L2-resident (one result bit per record slot) and the
  *                       bits are gathered back into key order.  Same answers
  *                       (a key's answer depends only on its block and
- *                       pattern).  Uses the range size and batch limit
- *                       of bf_set_add_mode and the same filter-owned scratch
+ *                       pattern).  Uses the range size (default 64
+ *                       MiB) and batch limit of bf_set_add_mode and the same filter-owned scratch
  *                       (+ 4 bytes per key of a batch for the slots and one
  *                       bit per record slot), serialised with the binned add
  *                       the same way.
