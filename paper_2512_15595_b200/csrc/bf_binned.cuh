@@ -49,6 +49,16 @@ struct BinParams {
     uint32_t* res_bits;
 };
 
+// Programmatic dependent launch of the per-range kernels (apply, lookup):
+// ranges are independent (OR commutes; a lookup reads the filter and writes
+// its own result words), so launch r+1 may start while launch r drains.  Each
+// kernel lets its dependent launch as soon as all its CTAs are running, and
+// waits for its prerequisite only before it exits, so launches still COMPLETE
+// in stream order (what the kernels after the last range rely on).  Both are
+// no-ops in a launch without the programmatic attribute.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait_prerequisite() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // 512 threads x 8 keys: 177-180 Gkeys/s for the bin phase at R = 256 vs 162-166
 // for 256 x 16 and 155 for the r1 kernel (tools/kexp bin2, profiles/r2_kexp.md)
 constexpr int BIN_THREADS = 512;
@@ -594,6 +604,7 @@ __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
 {
     using W = typename C::W;
     constexpr int KPT = C::KPT;
+    pdl_launch_dependents();
     constexpr uint64_t TILE = 32 * KPT;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t pos = lane & (uint32_t)(C::THETA - 1);
@@ -651,6 +662,7 @@ __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
             }
         }
     }
+    pdl_wait_prerequisite();
 }
 
 // ---------------------------------------------------------------------------
@@ -671,6 +683,7 @@ __global__ void __launch_bounds__(256) lookup_kernel(const BinParams bp)
 {
     using W = typename C::W;
     constexpr int RK = LOOKUP_RPL;
+    pdl_launch_dependents();
     constexpr uint64_t TILE = 32 * RK;
     SaltSrc<C> ss;
     ss.init(0, nullptr, nullptr);
@@ -707,6 +720,7 @@ __global__ void __launch_bounds__(256) lookup_kernel(const BinParams bp)
         }
         if (lane < (uint32_t)RK) res[s0 / 32 + lane] = mine;
     }
+    pdl_wait_prerequisite();
 }
 
 // Key order again: bit i of the batch's result words = the result bit of
