@@ -75,6 +75,36 @@ def test_instantiation_table_matches_generator(bflib):
         assert (0, v, B, S, k, z, th, ph, 4, 0) in inst and (1, v, B, S, k, z, 1, s, 4, 0) in inst
 
 
+def test_registry_keys_are_collision_free():
+    """Every generated kernel (bulk schedules, binned add / contains, routing,
+    draw schemes) packs to a distinct registry key with the library's field
+    layout (bf_internal.h InstKey::pack: op 4 bits, variant 3, B/32 6, S 1,
+    k 6, z 6, Θ 6, Φ 6, KPT 4, hv 4, scheme 2).  The library also aborts at
+    load on a collision; this checks the layout's field widths directly."""
+    import importlib.util
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location(
+        "gen_instances", os.path.join(here, "paper_2512_15595_b200", "csrc", "gen_instances.py"))
+    g = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(g)
+    inst = g.instances()
+    binned = []
+    for op, v, B, S, k, z, theta, phi, kpt, hv in [i[:10] for i in inst]:
+        if op == 0 and (theta, phi) == g.default_add(v, B, S, z) and kpt == 4 and hv == 0:
+            for bop, t2, p2, k2 in ((2, 1, 1, 1), (6, 1, 1, 1), (3, theta, phi, kpt), (4, 1, B // S, 1),
+                                    (7, 1, 1, 1), (8, 1, B // S, 1), (9, 1, B // S, 1)):
+                binned.append((bop, v, B, S, k, z, t2, p2, k2, hv))
+    allk = [i if len(i) > 10 else tuple(i) + (0,) for i in inst + binned]
+
+    def pack(op, v, B, S, k, z, th, ph, kpt, hv, hs):
+        assert op < 16 and v < 8 and B // 32 < 64 and k < 64 and z < 64 and th < 64 and ph < 64 and kpt < 16 \
+            and hv < 16 and hs < 4
+        return (op | v << 4 | (B // 32) << 7 | (S == 64) << 13 | k << 14 | z << 20 | th << 26 | ph << 32
+                | kpt << 38 | hv << 42 | hs << 46)
+    keys = [pack(*i[:11]) for i in allk]
+    assert len(set(keys)) == len(set(allk))
+
+
 def _build_demo():
     import shutil
     import subprocess
@@ -158,6 +188,14 @@ def test_null_handle_calls_fail_cleanly(bflib):
     L.bf_add.restype = ctypes.c_int
     L.bf_add.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
     assert L.bf_add(None, None, 10, None) == bflib.BF_EINVAL
+    for name in ("bf_set_contains_mode", "bf_set_add_mode"):
+        fn = getattr(L, name)
+        fn.restype = ctypes.c_int
+    L.bf_set_contains_mode.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    assert L.bf_set_contains_mode(None, 0) == bflib.BF_EINVAL
+    L.bf_get_contains_mode.restype = ctypes.c_int
+    L.bf_get_contains_mode.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    assert L.bf_get_contains_mode(None, None, None) == bflib.BF_EINVAL
     L.bf_destroy.argtypes = [ctypes.c_void_p]
     L.bf_destroy(None)  # NULL-safe
     assert bflib.last_error()[0] in (bflib.BF_EINVAL, bflib.BF_OK)
