@@ -299,30 +299,25 @@ __global__ void __launch_bounds__(NT) bin_kernel(const BinParams bp)
 //     of chunk c+1 between its own barriers;
 //   * keys are loaded 256 bits at a time (KPT consecutive keys per thread;
 //     the order of records inside a bucket run is free: OR commutes).
-// Shared memory: stage[CHUNK] u64 | cnt[2][Rp] u32 | rbase[Rp] u32 | flags.
+// Shared memory: stage[2][CHUNK] u64 | cnt[2][Rp] u32 | rbase[2][Rp] u32 | flags[2].
 __host__ __device__ inline size_t bin_range_smem_bytes(uint32_t nranges, uint32_t chunk = BIN_CHUNK)
 {
     const size_t rp = (nranges + 3) & ~3u;
-    return (size_t)chunk * 8 + rp * 4 * 3 + 16;
+    return (size_t)chunk * 8 * 2 + rp * 4 * 4 + 16;
 }
 
-template <class C1, int NT, int KPT, bool FULL, bool SLOTS>
-__device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, uint32_t cnt, uint32_t R,
-                                                uint32_t chunk_no, uint64_t* stage, uint32_t* cnt2, uint32_t* rbase,
-                                                uint32_t* flags, uint32_t* warp_tot, const SaltSrc<C1>& ss,
-                                                uint64_t* const recs, unsigned long long* const cursor,
-                                                const uint32_t cap, const uint64_t seed, const uint32_t b32,
-                                                const uint32_t lg_bpr, const uint64_t pol, uint32_t* const slot_out)
+// The phases of one chunk (bin_range_kernel runs them software-pipelined:
+// the key loads and hashing of chunk i+1 share a phase with the write-out of
+// chunk i).  Buffers x = chunk index & 1: hist[x] (counters, then run
+// offsets), rbase[x], stage[x], flags[x].
+// (a) load KPT consecutive keys (issued first: the previous chunk's
+// write-out runs while they are in flight), then hash them and rank each in
+// its bucket's counter
+template <int KPT, bool FULL>
+__device__ __forceinline__ void rb_load(const uint64_t* keys, uint64_t base, uint32_t cnt, uint64_t (&key)[KPT])
 {
-    using W = typename C1::W;
-    constexpr int CHUNK = NT * KPT;
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t Rp = (R + 3) & ~3u;
-    uint32_t* hist = cnt2 + (chunk_no & 1u) * Rp;           // this chunk's counters (zeroed by the previous chunk)
-    uint32_t* hnext = cnt2 + ((chunk_no & 1u) ^ 1u) * Rp;   // the next chunk's
-    // (a) load KPT consecutive keys, hash, rank in the bucket's counter
-    uint64_t key[KPT];
-    const uint64_t* kp = p.keys + base + (uint64_t)tid * KPT;
+    const uint32_t tid = threadIdx.x;
+    const uint64_t* kp = keys + base + (uint64_t)tid * KPT;
     if (FULL) {
 #pragma unroll
         for (int i = 0; i < KPT; i += 4) {
@@ -335,10 +330,16 @@ __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, 
 #pragma unroll
         for (int i = 0; i < KPT; ++i) key[i] = (tid * KPT + i < cnt) ? ld_key1(kp + i) : 0ULL;
     }
-    uint64_t rec[KPT];
-    uint32_t rl[KPT];  // (bucket << 16) | rank
+}
+
+template <int KPT, bool FULL>
+__device__ __forceinline__ void rb_rank(const uint64_t (&key)[KPT], uint32_t cnt, uint32_t* hist, uint64_t seed,
+                                        uint32_t b32, uint32_t lg_bpr, uint64_t (&rec)[KPT], uint32_t (&rl)[KPT])
+{
+    const uint32_t tid = threadIdx.x;
 #pragma unroll
     for (int i = 0; i < KPT; ++i) {
+        rl[i] = 0;
         if (FULL || tid * KPT + i < cnt) {
             const uint64_t h = xxh64_u64(key[i], seed);
             const uint32_t blk = block_of(h, b32);
@@ -347,13 +348,21 @@ __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, 
             rl[i] = (r << 16) | atomicAdd(&hist[r], 1u);
         }
     }
-    __syncthreads();
-    // (b) reserve each bucket's run (one global atomic per touched bucket),
-    // exclusive scan of the counts -> run offsets; rbase[r] = r*cap + base - offset
-    // Buckets per thread: one when R <= NT (the common case: every
-    // reservation of the chunk in flight at once), else ceil(R / NT)
-    // consecutive ones.  The reserved base waits in rbase[r] across the
-    // barrier.  Only the warps that own buckets scan.
+}
+
+// (b) reserve each bucket's run (one global atomic per touched bucket),
+// exclusive scan of the counts -> run offsets in hist; rbase[r] = r*cap +
+// reserved base - offset; zero hfree (the counters of the chunk after next).
+// Buckets per thread: one when R <= NT (the common case: every reservation
+// of the chunk in flight at once), else ceil(R / NT) consecutive ones (the
+// reserved base waits in rbase[r] across the barrier).  Only the warps that
+// own buckets scan.  Contains one barrier.
+template <int NT>
+__device__ __forceinline__ void rb_reserve(uint32_t R, uint32_t* hist, uint32_t* rbase, uint32_t* hfree,
+                                           uint32_t* flag, uint32_t* warp_tot, unsigned long long* cursor,
+                                           uint32_t cap, uint32_t chunk_no)
+{
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t per = (R + NT - 1) / NT;
     const uint32_t r0 = tid * per, r1 = min(R, r0 + per);
     const uint32_t nscan = (R + per * 32 - 1) / (per * 32);  // warps that own buckets
@@ -362,12 +371,12 @@ __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, 
     if (per == 1) {
         if (tid < R) {
             c1 = hist[tid];
-            if constexpr (tuning::BIN_FAKE_RESERVE) {
+            if constexpr (tuning::BIN_FAKE_RESERVE) {  // experiment: no global atomic (wrong records, timing bound)
                 g1 = (blockIdx.x * 16 + (chunk_no & 15u)) * 16u % (cap / 2u);
             } else {
                 g1 = c1 ? (uint32_t)atomicAdd(cursor + tid, (unsigned long long)c1) : 0u;
             }
-            if (g1 + c1 > cap) flags[chunk_no & 1u] = 1u;
+            if (g1 + c1 > cap) *flag = 1u;
         }
         if (warp < nscan) {
             incl = c1;
@@ -383,7 +392,7 @@ __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, 
         for (uint32_t r = r0; r < r1; ++r) {
             const uint32_t c = hist[r];
             uint32_t g;
-            if constexpr (tuning::BIN_FAKE_RESERVE) {  // experiment: no global atomic (wrong records, timing bound)
+            if constexpr (tuning::BIN_FAKE_RESERVE) {
                 g = (blockIdx.x * 16 + (chunk_no & 15u)) * 16u % (cap / 2u);
             } else {
                 g = c ? (uint32_t)atomicAdd(cursor + r, (unsigned long long)c) : 0u;
@@ -399,7 +408,7 @@ __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, 
             if (lane >= (uint32_t)o) incl += v;
         }
         if (lane == 31) warp_tot[warp] = incl;
-        if (ovf) flags[chunk_no & 1u] = 1u;
+        if (ovf) *flag = 1u;
     }
     __syncthreads();
     if (per == 1) {
@@ -409,7 +418,7 @@ __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, 
             for (int w = 0; w < NT / 32; ++w) run += (uint32_t)w < warp ? warp_tot[w] : 0u;
             hist[tid] = run;
             rbase[tid] = tid * cap + g1 - run;
-            hnext[tid] = 0u;  // the next chunk's counters (last read by the previous chunk's (c))
+            hfree[tid] = 0u;
         }
     } else if (warp < nscan) {
         uint32_t run = incl - tot;
@@ -419,13 +428,20 @@ __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, 
             const uint32_t c = hist[r];
             hist[r] = run;
             rbase[r] = r * cap + rbase[r] - run;
-            hnext[r] = 0u;  // the next chunk's counters (last read by the previous chunk's (c))
+            hfree[r] = 0u;
             run += c;
         }
     }
-    __syncthreads();
-    // (c) sorted slots in shared memory (binned contains: and every key's
-    // record slot, rbase[r] + its sorted position, in key order)
+}
+
+// (c) sorted slots in shared memory (binned contains: and every key's record
+// slot, rbase[r] + its sorted position, in key order)
+template <int NT, int KPT, bool FULL, bool SLOTS>
+__device__ __forceinline__ void rb_scatter(uint64_t base, uint32_t cnt, const uint32_t* hist, const uint32_t* rbase,
+                                           uint64_t* stage, uint32_t cap, uint32_t* slot_out,
+                                           const uint64_t (&rec)[KPT], const uint32_t (&rl)[KPT])
+{
+    const uint32_t tid = threadIdx.x;
     uint32_t* const so = SLOTS ? slot_out + base + (uint64_t)tid * KPT : nullptr;
 #pragma unroll
     for (int i0 = 0; i0 < KPT; i0 += 4) {  // slots leave 4 at a time (16-byte stores, few live registers)
@@ -456,12 +472,20 @@ __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, 
             }
         }
     }
-    if (tid == 0) flags[(chunk_no & 1u) ^ 1u] = 0u;  // the next chunk's overflow flag
-    __syncthreads();
-    // (d) coalesced write-out: slot j of the chunk goes to rbase[range(stage[j])] + j
-    if (flags[chunk_no & 1u] == 0u) {
+}
+
+// (d) coalesced write-out: slot j of the chunk goes to rbase[range(stage[j])] + j
+// (slots i*NT + tid for i in [I0, I1): the write-out runs in two halves)
+template <class C1, int NT, int KPT, int I0, int I1, bool FULL, bool SLOTS>
+__device__ __forceinline__ void rb_write(const Params& p, uint32_t cnt, const uint64_t* stage, const uint32_t* rbase,
+                                         uint32_t flag, uint32_t cap, uint32_t lg_bpr, uint64_t* recs, uint64_t pol,
+                                         const SaltSrc<C1>& ss)
+{
+    using W = typename C1::W;
+    const uint32_t tid = threadIdx.x;
+    if (flag == 0u) {
 #pragma unroll
-        for (int i = 0; i < KPT; ++i) {
+        for (int i = I0; i < I1; ++i) {
             const uint32_t j = i * NT + tid;
             if (FULL || j < cnt) {
                 const uint64_t v = stage[j];
@@ -470,7 +494,7 @@ __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, 
         }
     } else {  // some bucket of this chunk is full (never with uniform hashes): OR its overflow directly
 #pragma unroll 1
-        for (int i = 0; i < KPT; ++i) {
+        for (int i = I0; i < I1; ++i) {
             const uint32_t j = i * NT + tid;
             if (FULL || j < cnt) {
                 const uint64_t v = stage[j];
@@ -483,20 +507,29 @@ __device__ __forceinline__ void bin_range_chunk(const Params& p, uint64_t base, 
     }
 }
 
+// Range binning, software-pipelined over the CTA's chunks (round 2b):
+//   prologue: load+rank(0) | barrier | reserve(0) | barrier | scatter(0) | barrier
+//   step i:   load(i+1), write(i) first half, rank(i+1) | barrier A |
+//             reservation atomics of (i+1), write(i) second half, scan of (i+1) |
+//             barrier B (inside the scan) | offsets | barrier C | scatter(i+1) | barrier D
+// so the key loads of the next chunk and its reservation atomics are in
+// flight while this chunk's records are stored.  Double buffers (x = chunk
+// & 1) for stage, counters, rbase and the overflow flag; each is rewritten
+// only after a barrier that follows its last reader.
 template <class C1, int NT = BIN_THREADS, int KPT = BIN_KPT, int MINB = BIN_RANGE_MINB, bool SLOTS = false>
 __global__ void __launch_bounds__(NT, MINB) bin_range_kernel(const BinParams bp)
 {
-    constexpr int CHUNK = NT * KPT;
+    constexpr int CHUNK = NT * KPT, KH = KPT / 2;
     static_assert(CHUNK <= 65536 && KPT % 4 == 0, "u16 ranks, 256-bit key loads");
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t R = bp.nranges;
     const uint32_t Rp = (R + 3) & ~3u;
-    uint64_t* stage = (uint64_t*)smem;
-    uint32_t* cnt2 = (uint32_t*)(stage + CHUNK);
-    uint32_t* rbase = cnt2 + 2 * Rp;
-    uint32_t* flags = rbase + Rp;
+    uint64_t* stage2 = (uint64_t*)smem;                 // [2][CHUNK]
+    uint32_t* hist2 = (uint32_t*)(stage2 + 2 * CHUNK);  // [2][Rp]
+    uint32_t* rbase2 = hist2 + 2 * Rp;                  // [2][Rp]
+    uint32_t* flags = rbase2 + 2 * Rp;                  // [2]
     __shared__ uint32_t warp_tot[NT / 32];
-    for (uint32_t r = threadIdx.x; r < Rp; r += NT) cnt2[r] = 0u;
+    for (uint32_t r = threadIdx.x; r < 2 * Rp; r += NT) hist2[r] = 0u;
     if (threadIdx.x < 2) flags[threadIdx.x] = 0u;
     __syncthreads();
     SaltSrc<C1> ss;
@@ -508,24 +541,111 @@ __global__ void __launch_bounds__(NT, MINB) bin_range_kernel(const BinParams bp)
     unsigned long long* const cursor = bp.cursor;
     const uint64_t pol = l2_evict_first_policy();
     const bool vec_ok = ((uintptr_t)p.keys & 31u) == 0;
-    uint32_t chunk_no = 0;
-    for (uint64_t c = blockIdx.x; c * CHUNK < n; c += gridDim.x, ++chunk_no) {
-        const uint64_t base = c * CHUNK;
-        const uint32_t cnt = (uint32_t)min((uint64_t)CHUNK, n - base);
-        {  // L2 prefetch of this CTA's next chunk (one grid stride ahead)
-            const uint64_t pb = base + (uint64_t)gridDim.x * CHUNK;
-            for (uint32_t l = threadIdx.x; l < CHUNK / 16; l += NT) {
-                const uint64_t q = pb + (uint64_t)l * 16;
-                if (q < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.keys + q));
-            }
+    const uint64_t nchunks = (n + CHUNK - 1) / CHUNK;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const bool one = R <= (uint32_t)NT;                 // one bucket per thread (the common case)
+    const uint32_t nscan1 = (R + 31) / 32;              // warps that own buckets when `one`
+    uint64_t c = blockIdx.x;
+    if (c >= nchunks) return;
+    auto cnt_of = [&](uint64_t ch) { return (uint32_t)min((uint64_t)CHUNK, n - ch * CHUNK); };
+    auto prefetch_after = [&](uint64_t ch) {  // L2 prefetch of the chunk after ch (one grid stride ahead)
+        const uint64_t pb = (ch + gridDim.x) * CHUNK;
+        for (uint32_t l = threadIdx.x; l < CHUNK / 16; l += NT) {
+            const uint64_t q = pb + (uint64_t)l * 16;
+            if (q < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.keys + q));
         }
-        if (cnt == CHUNK && vec_ok)
-            bin_range_chunk<C1, NT, KPT, true, SLOTS>(p, base, cnt, R, chunk_no, stage, cnt2, rbase, flags, warp_tot,
-                                                      ss, recs, cursor, cap, seed, b32, lg_bpr, pol, bp.slot_out);
+    };
+    auto write = [&](auto half, bool full_, uint32_t cnt_, uint32_t xb, uint32_t fl) {
+        constexpr int H = decltype(half)::value;  // 0: slots [0, KH), 1: [KH, KPT)
+        if (full_)
+            rb_write<C1, NT, KPT, H * KH, H * KH + KH, true, SLOTS>(p, cnt_, stage2 + xb * CHUNK, rbase2 + xb * Rp, fl,
+                                                                    cap, lg_bpr, recs, pol, ss);
         else
-            bin_range_chunk<C1, NT, KPT, false, SLOTS>(p, base, cnt, R, chunk_no, stage, cnt2, rbase, flags,
-                                                       warp_tot, ss, recs, cursor, cap, seed, b32, lg_bpr, pol,
-                                                       bp.slot_out);
+            rb_write<C1, NT, KPT, H * KH, H * KH + KH, false, SLOTS>(p, cnt_, stage2 + xb * CHUNK, rbase2 + xb * Rp, fl,
+                                                                     cap, lg_bpr, recs, pol, ss);
+    };
+    uint64_t key[KPT], rec[KPT];
+    uint32_t rl[KPT];
+    // prologue: chunk 0 of this CTA up to its sorted stage
+    uint32_t x = 0, cnt = cnt_of(c);
+    bool full = cnt == CHUNK && vec_ok;
+    prefetch_after(c);
+    if (full) {
+        rb_load<KPT, true>(p.keys, c * CHUNK, cnt, key);
+        rb_rank<KPT, true>(key, cnt, hist2, seed, b32, lg_bpr, rec, rl);
+    } else {
+        rb_load<KPT, false>(p.keys, c * CHUNK, cnt, key);
+        rb_rank<KPT, false>(key, cnt, hist2, seed, b32, lg_bpr, rec, rl);
+    }
+    __syncthreads();
+    rb_reserve<NT>(R, hist2, rbase2, hist2 + Rp, &flags[0], warp_tot, cursor, cap, 0);
+    __syncthreads();
+    if (full) rb_scatter<NT, KPT, true, SLOTS>(c * CHUNK, cnt, hist2, rbase2, stage2, cap, bp.slot_out, rec, rl);
+    else rb_scatter<NT, KPT, false, SLOTS>(c * CHUNK, cnt, hist2, rbase2, stage2, cap, bp.slot_out, rec, rl);
+    __syncthreads();
+    for (uint32_t i = 0;; ++i, x ^= 1u) {
+        const uint64_t cn = c + gridDim.x;
+        const bool more = cn < nchunks;
+        const uint32_t y = x ^ 1u;
+        const uint32_t fl = flags[x];
+        if (!more) {
+            write(std::integral_constant<int, 0>{}, full, cnt, x, fl);
+            write(std::integral_constant<int, 1>{}, full, cnt, x, fl);
+            break;
+        }
+        const uint32_t cntn = cnt_of(cn);
+        const bool fulln = cntn == CHUNK && vec_ok;
+        uint32_t* const hy = hist2 + y * Rp;
+        uint32_t* const ry = rbase2 + y * Rp;
+        prefetch_after(cn);
+        if (fulln) rb_load<KPT, true>(p.keys, cn * CHUNK, cntn, key);
+        else rb_load<KPT, false>(p.keys, cn * CHUNK, cntn, key);
+        write(std::integral_constant<int, 0>{}, full, cnt, x, fl);  // while the keys arrive
+        if (fulln) rb_rank<KPT, true>(key, cntn, hy, seed, b32, lg_bpr, rec, rl);
+        else rb_rank<KPT, false>(key, cntn, hy, seed, b32, lg_bpr, rec, rl);
+        __syncthreads();  // A: the next chunk's counts are complete
+        if (one) {
+            uint32_t c1 = 0, g1 = 0;
+            if (tid < R) {
+                c1 = hy[tid];
+                if constexpr (tuning::BIN_FAKE_RESERVE) {  // experiment: no global atomic (wrong records, a bound)
+                    g1 = (blockIdx.x * 16 + ((i + 1) & 15u)) * 16u % (cap / 2u);
+                } else {
+                    g1 = c1 ? (uint32_t)atomicAdd(cursor + tid, (unsigned long long)c1) : 0u;
+                }
+            }
+            write(std::integral_constant<int, 1>{}, full, cnt, x, fl);  // while the reservations return
+            uint32_t incl = c1;
+            if (warp < nscan1) {
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= (uint32_t)o) incl += v;
+                }
+                if (lane == 31) warp_tot[warp] = incl;
+            }
+            if (tid < R && g1 + c1 > cap) flags[y] = 1u;
+            __syncthreads();  // B
+            if (tid < R) {
+                uint32_t run = incl - c1;
+#pragma unroll
+                for (int w = 0; w < NT / 32; ++w) run += (uint32_t)w < warp ? warp_tot[w] : 0u;
+                hy[tid] = run;
+                ry[tid] = tid * cap + g1 - run;
+                hist2[x * Rp + tid] = 0u;  // chunk i+2's counters (last read by scatter(i), a step ago)
+            }
+        } else {
+            write(std::integral_constant<int, 1>{}, full, cnt, x, fl);
+            rb_reserve<NT>(R, hy, ry, hist2 + x * Rp, &flags[y], warp_tot, cursor, cap, i + 1);
+        }
+        __syncthreads();  // C
+        if (fulln) rb_scatter<NT, KPT, true, SLOTS>(cn * CHUNK, cntn, hy, ry, stage2 + y * CHUNK, cap, bp.slot_out, rec, rl);
+        else rb_scatter<NT, KPT, false, SLOTS>(cn * CHUNK, cntn, hy, ry, stage2 + y * CHUNK, cap, bp.slot_out, rec, rl);
+        if (tid == 0) flags[x] = 0u;  // chunk i+2's flag (read above, before three barriers)
+        __syncthreads();  // D
+        c = cn;
+        cnt = cntn;
+        full = fulln;
     }
 }
 
