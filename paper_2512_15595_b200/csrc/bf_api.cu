@@ -4,7 +4,6 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
-#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -580,36 +579,6 @@ static bool binned_available(const bf_filter* f, KernelFn* bin, KernelFn* apply)
 static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cudaStream_t st, KernelFn bin_fn,
                              KernelFn apply_fn);
 
-static uint32_t env_int(const char* name, int dflt)
-{
-    const char* s = getenv(name);
-    const int v = s ? atoi(s) : dflt;
-    return (uint32_t)(v > 0 ? v : dflt);
-}
-
-// Lookup phase launch form of the binned contains, as apply_all_ctas_per_sm
-// (experiment knob BF200_LOOKUP_CPS, read once; 0 = one launch per range).
-static int lookup_all_ctas_per_sm()
-{
-    static const int v = [] {
-        const char* s = getenv("BF200_LOOKUP_CPS");
-        return s ? atoi(s) : 0;
-    }();
-    return v;
-}
-
-// Apply phase launch form: resident CTAs per SM of the single all-ranges
-// apply launch, 0 = one launch per range.  Experiment knob
-// BF200_APPLY_CPS (read once).
-static int apply_all_ctas_per_sm()
-{
-    static const int v = [] {
-        const char* s = getenv("BF200_APPLY_CPS");
-        return s ? atoi(s) : 0;
-    }();
-    return v;
-}
-
 static int binned_add(bf_filter* f, const uint64_t* keys, uint64_t n, cudaStream_t st, KernelFn bin_fn,
                       KernelFn apply_fn)
 {
@@ -685,15 +654,15 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         }
         f->recs_bytes = need;
     }
-    if (f->cursor_n < 4 * R) {  // per buffer: R reservation counters + R apply tickets
+    if (f->cursor_n < 2 * R) {
         if (f->cursor) cudaFree(f->cursor);
         f->cursor = nullptr;
-        e = cudaMalloc(&f->cursor, 4 * R * sizeof(unsigned long long));
+        e = cudaMalloc(&f->cursor, 2 * R * sizeof(unsigned long long));
         if (e != cudaSuccess) {
             cudaGetLastError();
             return fail(BF_ENOMEM, "binned add counters: %s", cudaGetErrorString(e));
         }
-        f->cursor_n = (uint32_t)(4 * R);
+        f->cursor_n = (uint32_t)(2 * R);
     }
     if (tuning::BINNED_OVERLAP && !f->side) {  // the apply stream and the pipeline's events (once per filter)
         if ((e = cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking)) != cudaSuccess)
@@ -709,7 +678,6 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
     // waves of CTAs like the bulk kernels (bin phase 178 -> 180 Gkeys/s vs the occupancy grid, tools/kexp bin2)
     const int grid_bin = kWaveCtasPerSm * sm_count(f->device);
     const int grid_apply = kWaveCtasPerSm * sm_count(f->device);
-    const int apply_cps = apply_all_ctas_per_sm();
     cudaStream_t side = tuning::BINNED_OVERLAP ? f->side : st;
     uint64_t i = 0;
     for (uint64_t off = 0; off < n; off += batch, ++i) {
@@ -719,7 +687,7 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         memset(&bp, 0, sizeof bp);
         bp.f = make_params(f, keys + off, cnt, nullptr);
         bp.recs = f->recs + buf * per_buf;
-        bp.cursor = f->cursor + buf * 2 * R;
+        bp.cursor = f->cursor + buf * R;
         bp.cap = cap;
         bp.lg_bpr = lg;
         bp.nranges = (uint32_t)R;
@@ -727,7 +695,7 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         // the buffer is free once the apply of batch i-2 has read it
         if (side != st && i >= 2 && (e = cudaStreamWaitEvent(st, f->ev_apply[buf], 0)) != cudaSuccess)
             return cuda_fail(e, "binned add: wait for the buffer");
-        if ((e = cudaMemsetAsync(bp.cursor, 0, 2 * R * sizeof(unsigned long long), st)) != cudaSuccess)
+        if ((e = cudaMemsetAsync(bp.cursor, 0, R * sizeof(unsigned long long), st)) != cudaSuccess)
             return cuda_fail(e, "binned add: cursor reset");
         void* args[] = {&bp};
         uint64_t chunks = (cnt + BIN_CHUNK - 1) / BIN_CHUNK;
@@ -738,26 +706,15 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         if (side != st && ((e = cudaEventRecord(f->ev_bin[buf], st)) != cudaSuccess ||
                            (e = cudaStreamWaitEvent(side, f->ev_bin[buf], 0)) != cudaSuccess))
             return cuda_fail(e, "binned add: bin -> apply");
-        if (apply_cps > 0) {
-            // one launch for all ranges, range-major through per-range tickets
-            bp.tickets = bp.cursor + R;
-            bp.tchunk = env_int("BF200_APPLY_CHUNK", 8);
-            if ((e = launch_range_kernel(apply_fn, (unsigned)(apply_cps * sm_count(f->device)), args, side, false)) !=
-                cudaSuccess)
+        // one launch per range: the GPU stays inside one L2-resident range
+        const uint64_t tiles = (cap + 32 * f->sched[0].kpt - 1) / (32 * f->sched[0].kpt);
+        uint64_t ga = (tiles + 7) / 8;
+        if (ga > (uint64_t)grid_apply) ga = grid_apply;
+        for (uint32_t r = 0; r < (uint32_t)R; ++r) {
+            bp.range = r;
+            if ((e = launch_range_kernel(apply_fn, (unsigned)ga, args, side, r > 0)) != cudaSuccess)
                 return cuda_fail(e, "apply launch");
             if (int rc = check_launch("apply launch")) return rc;
-            bp.tickets = nullptr;
-        } else {
-            // one launch per range: the GPU stays inside one L2-resident range
-            const uint64_t tiles = (cap + 32 * f->sched[0].kpt - 1) / (32 * f->sched[0].kpt);
-            uint64_t ga = (tiles + 7) / 8;
-            if (ga > (uint64_t)grid_apply) ga = grid_apply;
-            for (uint32_t r = 0; r < (uint32_t)R; ++r) {
-                bp.range = r;
-                if ((e = launch_range_kernel(apply_fn, (unsigned)ga, args, side, r > 0)) != cudaSuccess)
-                    return cuda_fail(e, "apply launch");
-                if (int rc = check_launch("apply launch")) return rc;
-            }
         }
         if (side != st && (e = cudaEventRecord(f->ev_apply[buf], side)) != cudaSuccess)
             return cuda_fail(e, "binned add: apply event");
@@ -841,7 +798,6 @@ static int binned_contains_locked(bf_filter* f, const uint64_t* keys, uint64_t n
     const size_t smem = bin_range_smem_bytes((uint32_t)R);
     cudaFuncSetAttribute((const void*)bin_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int waves = kWaveCtasPerSm * sm_count(f->device);
-    const int lookup_cps = lookup_all_ctas_per_sm();
     for (uint64_t off = 0; off < n; off += batch) {
         const uint64_t cnt = n - off < batch ? n - off : batch;
         BinParams bp;
@@ -854,7 +810,7 @@ static int binned_contains_locked(bf_filter* f, const uint64_t* keys, uint64_t n
         bp.nranges = (uint32_t)R;
         bp.slot_out = f->slots;
         bp.res_bits = f->resb;
-        if ((e = cudaMemsetAsync(bp.cursor, 0, 2 * R * sizeof(unsigned long long), st)) != cudaSuccess)
+        if ((e = cudaMemsetAsync(bp.cursor, 0, R * sizeof(unsigned long long), st)) != cudaSuccess)
             return cuda_fail(e, "binned contains: cursor reset");
         void* args[] = {&bp};
         const uint64_t chunks = (cnt + BIN_CHUNK - 1) / BIN_CHUNK;
@@ -865,21 +821,11 @@ static int binned_contains_locked(bf_filter* f, const uint64_t* keys, uint64_t n
         const uint64_t tiles = (cap + 32 * LOOKUP_RPL - 1) / (32 * LOOKUP_RPL);
         uint64_t gl = (tiles + 7) / 8;
         if (gl > (uint64_t)kLookupCtasPerSm * sm_count(f->device)) gl = (uint64_t)kLookupCtasPerSm * sm_count(f->device);
-        if (lookup_cps > 0) {  // one launch for all ranges, range-major through per-range tickets
-            bp.tickets = bp.cursor + R;
-            bp.tchunk = env_int("BF200_LOOKUP_CHUNK", 8);
-            if ((e = launch_range_kernel(look_fn, (unsigned)(lookup_cps * sm_count(f->device)), args, st, false)) !=
-                cudaSuccess)
+        for (uint32_t r = 0; r < (uint32_t)R; ++r) {  // one launch per range: the GPU stays in one L2-resident range
+            bp.range = r;
+            if ((e = launch_range_kernel(look_fn, (unsigned)gl, args, st, r > 0)) != cudaSuccess)
                 return cuda_fail(e, "binned contains: lookup launch");
             if ((rc = check_launch("binned contains: lookup launch"))) return rc;
-            bp.tickets = nullptr;
-        } else {
-            for (uint32_t r = 0; r < (uint32_t)R; ++r) {  // one launch per range: the GPU stays in one L2-resident range
-                bp.range = r;
-                if ((e = launch_range_kernel(look_fn, (unsigned)gl, args, st, r > 0)) != cudaSuccess)
-                    return cuda_fail(e, "binned contains: lookup launch");
-                if ((rc = check_launch("binned contains: lookup launch"))) return rc;
-            }
         }
         uint32_t* o = out + off / 32;  // off is a multiple of 128
         void* uargs[] = {&bp, &o};

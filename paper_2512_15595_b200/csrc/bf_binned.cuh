@@ -47,11 +47,6 @@ struct BinParams {
     // 0xFFFFFFFF = its bucket was full) and one result bit per record slot
     uint32_t* slot_out;
     uint32_t* res_bits;
-    // phase 2, one launch for ALL ranges of a batch (apply_kernel): per-range
-    // ticket counters (zeroed per batch) hand out chunks of APPLY_CHUNK tiles
-    // range by range; null: apply the single range bp.range
-    unsigned long long* tickets;
-    uint32_t tchunk;  // tiles per ticket
 };
 
 // Programmatic dependent launch of the per-range kernels (apply, lookup):
@@ -719,68 +714,11 @@ __device__ __forceinline__ void apply_tma_warp(const BinParams& bp, typename C::
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
-// Phase 2, the records of one tile (TILE = 32 * KPT records of bucket r,
-// `cnt` records in all) ORed into the filter with the add schedule of C.
-template <class C>
-__device__ __forceinline__ void apply_tile(const BinParams& bp, typename C::W* F, uint64_t r, uint64_t lt,
-                                           uint64_t cnt, uint32_t lane, uint32_t pos, uint32_t gbase,
-                                           const SaltSrc<C>& ss)
-{
-    constexpr int KPT = C::KPT;
-    constexpr uint64_t TILE = 32 * KPT;
-    const uint64_t* rp = bp.recs + r * bp.cap + lt * TILE + (uint64_t)lane * KPT;
-    const uint64_t left = cnt - lt * TILE;
-    uint64_t rec[KPT];
-    bool valid[KPT];
-    if (left >= TILE) {
-        uint64_t k[KPT];
-        load_tile_keys<KPT>(rp, 0, true, k);
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) {
-            rec[j] = k[j];
-            valid[j] = true;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) {
-            valid[j] = (uint64_t)lane * KPT + j < left;
-            rec[j] = valid[j] ? ld_key1(rp + j) : 0ULL;
-        }
-    }
-    if constexpr (C::THETA == 1) {
-#pragma unroll
-        for (int j = 0; j < KPT; ++j)
-            if (valid[j]) add_part<C>(F, (uint32_t)rec[j], (uint32_t)(rec[j] >> 32) - bp.blk_base, 0, ss);
-    } else {
-#pragma unroll 1
-        for (int rr = 0; rr < C::THETA; ++rr) {
-            const uint32_t src = gbase + rr;
-#pragma unroll
-            for (int j = 0; j < KPT; ++j) {
-                const uint32_t l = __shfl_sync(0xffffffffu, (uint32_t)rec[j], src);
-                const uint32_t bk = __shfl_sync(0xffffffffu, (uint32_t)(rec[j] >> 32) - bp.blk_base, src);
-                const bool v = __shfl_sync(0xffffffffu, (int)valid[j], src);
-                if (v) add_part<C>(F, l, bk, pos, ss);
-            }
-        }
-    }
-}
-
-// tiles per ticket of the all-ranges apply (one atomic per 8 x 128 records)
-constexpr uint32_t APPLY_CHUNK = 8;
-
-// Phase 2: apply the buckets range-major, so the whole GPU works inside one
-// L2-resident filter range at a time (a static grid-stride pass over all
-// buckets lets warps drift several ranges apart and the working set falls
-// out of L2: measured 10% RED hit rate vs ~90% expected).  Two launch forms:
-//  * bp.tickets == null: ONE bucket (bp.range) per launch, the host launches
-//    the ranges one after another (PDL between them);
-//  * bp.tickets != null: ONE launch for all buckets of the batch.  A warp
-//    takes chunks of APPLY_CHUNK tiles from range r's ticket counter and
-//    moves to range r+1 only when r's tiles are all handed out, so the
-//    in-flight window stays within about one range without the per-launch
-//    ramp and tail of 256 launches per batch.  The next ticket is requested
-//    before the current chunk is applied (its latency hides behind the REDs).
+// Phase 2: apply ONE bucket (bp.range) with the add schedule of C.  The host
+// launches the ranges one after another, so the whole GPU works inside one
+// L2-resident filter range at a time (a single grid-stride pass over all
+// buckets lets fast SMs drift several ranges ahead and the working set falls
+// out of L2: measured 10% RED hit rate vs ~90% expected).
 template <class C>
 __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
 {
@@ -796,32 +734,6 @@ __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     W* F = (W*)bp.f.words;
-    if (bp.tickets) {
-        uint32_t r = 0;
-        uint64_t cnt = min((uint64_t)bp.cursor[0], bp.cap);
-        uint64_t ntile = (cnt + TILE - 1) / TILE;
-        unsigned long long tk = 0;
-        if (lane == 0) tk = atomicAdd(bp.tickets, 1ULL);
-        tk = __shfl_sync(0xffffffffu, tk, 0);
-        for (;;) {
-            const uint64_t t0 = tk * bp.tchunk;
-            if (t0 >= ntile) {  // range r handed out: on to the next one
-                if (++r >= bp.nranges) break;
-                cnt = min((uint64_t)bp.cursor[r], bp.cap);
-                ntile = (cnt + TILE - 1) / TILE;
-                if (lane == 0) tk = atomicAdd(bp.tickets + r, 1ULL);
-                tk = __shfl_sync(0xffffffffu, tk, 0);
-                continue;
-            }
-            unsigned long long nxt = 0;
-            if (lane == 0) nxt = atomicAdd(bp.tickets + r, 1ULL);
-            const uint64_t t1 = min(t0 + bp.tchunk, ntile);
-            for (uint64_t lt = t0; lt < t1; ++lt) apply_tile<C>(bp, F, r, lt, cnt, lane, pos, gbase, ss);
-            tk = __shfl_sync(0xffffffffu, nxt, 0);
-        }
-        pdl_wait_prerequisite();
-        return;
-    }
     const uint64_t r = bp.range;
     const uint64_t cnt = min((uint64_t)bp.cursor[r], bp.cap);
     const uint64_t ntile = (cnt + TILE - 1) / TILE;
@@ -832,7 +744,44 @@ __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
             return;
         }
     }
-    for (uint64_t lt = gw; lt < ntile; lt += nw) apply_tile<C>(bp, F, r, lt, cnt, lane, pos, gbase, ss);
+    for (uint64_t lt = gw; lt < ntile; lt += nw) {
+        const uint64_t* rp = bp.recs + r * bp.cap + lt * TILE + (uint64_t)lane * KPT;
+        const uint64_t left = cnt - lt * TILE;
+        uint64_t rec[KPT];
+        bool valid[KPT];
+        if (left >= TILE) {
+            uint64_t k[KPT];
+            load_tile_keys<KPT>(rp, 0, true, k);
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) {
+                rec[j] = k[j];
+                valid[j] = true;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) {
+                valid[j] = (uint64_t)lane * KPT + j < left;
+                rec[j] = valid[j] ? ld_key1(rp + j) : 0ULL;
+            }
+        }
+        if constexpr (C::THETA == 1) {
+#pragma unroll
+            for (int j = 0; j < KPT; ++j)
+                if (valid[j]) add_part<C>(F, (uint32_t)rec[j], (uint32_t)(rec[j] >> 32) - bp.blk_base, 0, ss);
+        } else {
+#pragma unroll 1
+            for (int rr = 0; rr < C::THETA; ++rr) {
+                const uint32_t src = gbase + rr;
+#pragma unroll
+                for (int j = 0; j < KPT; ++j) {
+                    const uint32_t l = __shfl_sync(0xffffffffu, (uint32_t)rec[j], src);
+                    const uint32_t bk = __shfl_sync(0xffffffffu, (uint32_t)(rec[j] >> 32) - bp.blk_base, src);
+                    const bool v = __shfl_sync(0xffffffffu, (int)valid[j], src);
+                    if (v) add_part<C>(F, l, bk, pos, ss);
+                }
+            }
+        }
+    }
     pdl_wait_prerequisite();
 }
 
@@ -849,44 +798,6 @@ __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
 // directly by unbin_kernel.  C is the Θ = 1, Φ = s contains configuration.
 constexpr int LOOKUP_RPL = 4;  // records per lane per tile (loads in flight)
 
-// the records of one lookup tile (TILE = 32 * LOOKUP_RPL slots of bucket r)
-template <class C>
-__device__ __forceinline__ void lookup_tile(const BinParams& bp, const typename C::W* F, uint64_t r, uint64_t lt,
-                                            uint64_t cnt, uint32_t lane, const SaltSrc<C>& ss)
-{
-    using W = typename C::W;
-    constexpr int RK = LOOKUP_RPL;
-    constexpr uint64_t TILE = 32 * RK;
-    const uint64_t* rb = bp.recs + r * bp.cap;
-    uint32_t* res = bp.res_bits + (r * bp.cap) / 32;  // cap is a multiple of 128
-    const uint64_t s0 = lt * TILE;
-    uint64_t v[RK];
-    bool ok[RK];
-#pragma unroll
-    for (int j = 0; j < RK; ++j) {  // slot s0 + 32 j + lane: 256 contiguous bytes per warp load
-        ok[j] = s0 + 32 * j + lane < cnt;
-        v[j] = ok[j] ? ld_key1(rb + s0 + 32 * j + lane) : 0ULL;
-    }
-    W wd[RK][C::s];
-#pragma unroll
-    for (int j = 0; j < RK; ++j)
-        if (ok[j]) load_block<C>(F, (uint32_t)(v[j] >> 32) - bp.blk_base, wd[j]);
-    uint32_t mine = 0;
-#pragma unroll
-    for (int j = 0; j < RK; ++j) {
-        const bool hit = ok[j] && test_block<C>(wd[j], Draws<C>((uint32_t)v[j]), ss);
-        const uint32_t ball = __ballot_sync(0xffffffffu, hit);
-        if (lane == (uint32_t)j) mine = ball;
-    }
-    if (lane < (uint32_t)RK) res[s0 / 32 + lane] = mine;
-}
-
-// tiles per ticket of the all-ranges lookup
-constexpr uint32_t LOOKUP_CHUNK = 8;
-
-// The per-range lookup, in the same two launch forms as apply_kernel: one
-// range (bp.range) per launch, or all ranges of the batch in one launch
-// through per-range ticket counters (bp.tickets).
 template <class C>
 __global__ void __launch_bounds__(256) lookup_kernel(const BinParams bp)
 {
@@ -900,38 +811,35 @@ __global__ void __launch_bounds__(256) lookup_kernel(const BinParams bp)
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const W* F = (const W*)bp.f.words;
-    if (bp.tickets) {
-        uint32_t r = 0;
-        uint64_t cnt = min((uint64_t)bp.cursor[0], bp.cap);
-        uint64_t ntile = (cnt + TILE - 1) / TILE;
-        unsigned long long tk = 0;
-        if (lane == 0) tk = atomicAdd(bp.tickets, 1ULL);
-        tk = __shfl_sync(0xffffffffu, tk, 0);
-        for (;;) {
-            const uint64_t t0 = tk * bp.tchunk;
-            if (t0 >= ntile) {  // range r handed out: on to the next one
-                if (++r >= bp.nranges) break;
-                cnt = min((uint64_t)bp.cursor[r], bp.cap);
-                ntile = (cnt + TILE - 1) / TILE;
-                if (lane == 0) tk = atomicAdd(bp.tickets + r, 1ULL);
-                tk = __shfl_sync(0xffffffffu, tk, 0);
-                continue;
-            }
-            unsigned long long nxt = 0;
-            if (lane == 0) nxt = atomicAdd(bp.tickets + r, 1ULL);
-            const uint64_t t1 = min(t0 + bp.tchunk, ntile);
-            for (uint64_t lt = t0; lt < t1; ++lt) lookup_tile<C>(bp, F, r, lt, cnt, lane, ss);
-            tk = __shfl_sync(0xffffffffu, nxt, 0);
-        }
-        pdl_wait_prerequisite();
-        return;
-    }
     const uint64_t r = bp.range;
     const uint64_t cnt = min((uint64_t)bp.cursor[r], bp.cap);
     const uint64_t ntile = (cnt + TILE - 1) / TILE;
+    const uint64_t* rb = bp.recs + r * bp.cap;
+    uint32_t* res = bp.res_bits + (r * bp.cap) / 32;  // cap is a multiple of 128
     // (a software prefetch of the next tile's records measured slower: 74
     // registers, 11.0 -> 11.8 ms per 2^31 records; so did 2 and 8 records per lane)
-    for (uint64_t lt = gw; lt < ntile; lt += nw) lookup_tile<C>(bp, F, r, lt, cnt, lane, ss);
+    for (uint64_t lt = gw; lt < ntile; lt += nw) {
+        const uint64_t s0 = lt * TILE;
+        uint64_t v[RK];
+        bool ok[RK];
+#pragma unroll
+        for (int j = 0; j < RK; ++j) {  // slot s0 + 32 j + lane: 256 contiguous bytes per warp load
+            ok[j] = s0 + 32 * j + lane < cnt;
+            v[j] = ok[j] ? ld_key1(rb + s0 + 32 * j + lane) : 0ULL;
+        }
+        W wd[RK][C::s];
+#pragma unroll
+        for (int j = 0; j < RK; ++j)
+            if (ok[j]) load_block<C>(F, (uint32_t)(v[j] >> 32) - bp.blk_base, wd[j]);
+        uint32_t mine = 0;
+#pragma unroll
+        for (int j = 0; j < RK; ++j) {
+            const bool hit = ok[j] && test_block<C>(wd[j], Draws<C>((uint32_t)v[j]), ss);
+            const uint32_t ball = __ballot_sync(0xffffffffu, hit);
+            if (lane == (uint32_t)j) mine = ball;
+        }
+        if (lane < (uint32_t)RK) res[s0 / 32 + lane] = mine;
+    }
     pdl_wait_prerequisite();
 }
 
