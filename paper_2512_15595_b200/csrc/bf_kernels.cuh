@@ -321,33 +321,7 @@ __device__ __forceinline__ void load_block(const typename C::W* F, uint32_t blk,
 // instead of building and comparing masks; bit 0 of the AND of all tests is
 // the answer ("If any bit is zero, the element is certainly not in the
 // set").
-// The k draws of a BBF test, draw(J) for J in [0, K).  With EXIT (a whole
-// warp calls it, every lane with its own key) the draws run in groups of
-// tuning::EXIT_GROUP and the warp stops after a group once no lane's key has
-// all its tested bits set: every remaining draw could only AND more zeros
-// into acc ("If any bit is zero, the element is certainly not in the
-// set"), so the answers are those of the full test.
-template <class C, bool EXIT, class F>
-__device__ __forceinline__ void bbf_draws(const uint32_t& acc, F&& draw)
-{
-    constexpr int G = tuning::EXIT_GROUP;
-    if constexpr (EXIT && G > 0 && C::K > G) {
-        bool live = true;
-        StaticFor<0, (C::K + G - 1) / G>::run([&](auto GI) {
-            constexpr int g = decltype(GI)::value;
-            if constexpr (g > 0) {
-                if (live) live = __any_sync(0xffffffffu, acc & 1u);
-            }
-            if (live) {
-                StaticFor<g * G, (g * G + G < C::K ? g * G + G : C::K)>::run(draw);
-            }
-        });
-    } else {
-        StaticFor<0, C::K>::run(draw);
-    }
-}
-
-template <class C, bool EXIT = false>
+template <class C>
 __device__ __forceinline__ bool test_block(const typename C::W* wd, const Draws<C>& dr, const SaltSrc<C>& ss)
 {
     using W = typename C::W;
@@ -379,14 +353,14 @@ __device__ __forceinline__ bool test_block(const typename C::W* wd, const Draws<
         // s 64-bit words: bit p of the block = OR_i (w_i >> (p - 64 i)) with
         // PTX's clamping shifts (an amount >= 64, incl. a wrapped p - 64 i,
         // gives 0): no word select, no predicate
-        bbf_draws<C, EXIT>(acc, [&](auto J) {
+        StaticFor<0, C::K>::run([&](auto J) {
             const uint32_t p = top<C::LGB>(dr.template bbf_draw<decltype(J)::value>(ss));
             uint32_t t = shr_clamp_lo(wd[0], p);
             StaticFor<1, C::s>::run([&](auto I) { t |= shr_clamp_lo(wd[decltype(I)::value], p - 64u * decltype(I)::value); });
             acc &= t;
         });
     } else {  // BBF
-        bbf_draws<C, EXIT>(acc, [&](auto J) {
+        StaticFor<0, C::K>::run([&](auto J) {
             const uint32_t p = top<C::LGB>(dr.template bbf_draw<decltype(J)::value>(ss));
             const W x = (C::s > 1) ? pick<C::s>(wd, p >> C::LGW) : wd[0];
             acc &= (uint32_t)(x >> (p & (C::S - 1)));
@@ -401,7 +375,7 @@ __device__ __forceinline__ bool test_block(const typename C::W* wd, const Draws<
 // lanes' draws select.  Bit p of the block is bit (p & 31) of word p >> 5
 // (little-endian words): one LDS and one funnel rotate
 // per draw.  Each lane reads only what it wrote (program order, no barrier).
-template <class C, bool EXIT = false>
+template <class C>
 __device__ __forceinline__ bool test_block_sm(const typename C::W* wd, const Draws<C>& dr, const SaltSrc<C>& ss,
                                               uint32_t* col)
 {
@@ -412,7 +386,7 @@ __device__ __forceinline__ bool test_block_sm(const typename C::W* wd, const Dra
         else col[q * 32] = (uint32_t)wd[q];
     }
     uint32_t acc = 0xffffffffu;
-    bbf_draws<C, EXIT>(acc, [&](auto J) {
+    StaticFor<0, C::K>::run([&](auto J) {
         const uint32_t d = dr.template bbf_draw<decltype(J)::value>(ss);
         const uint32_t x = col[top<C::LGB - 5>(d) * 32];
         acc &= __funnelshift_r(x, x, top<C::LGB>(d));
@@ -632,11 +606,11 @@ __device__ __forceinline__ void run_tile(const Params& p, uint64_t tile, uint32_
         for (int j = 0; j < KPT; ++j) {
             if (FULL || valid[j]) {
                 if constexpr (C::BBF_SM && USE_SM)
-                    res |= (uint32_t)test_block_sm<C, FULL>(wd[j], Draws<C>::make(key[j], hfull[j], p.seed), ss,
-                                                            sm + j * (C::B / 32) * 32)
+                    res |= (uint32_t)test_block_sm<C>(wd[j], Draws<C>::make(key[j], hfull[j], p.seed), ss,
+                                                      sm + j * (C::B / 32) * 32)
                            << j;
                 else
-                    res |= (uint32_t)test_block<C, FULL>(wd[j], Draws<C>::make(key[j], hfull[j], p.seed), ss) << j;
+                    res |= (uint32_t)test_block<C>(wd[j], Draws<C>::make(key[j], hfull[j], p.seed), ss) << j;
             }
         }
     } else {

@@ -74,8 +74,5 @@ constexpr int APPLY_TMA_WARPS = 0;
 // experiment only (tools/kexp): the bin kernel's per-chunk run reservation
 // without the global atomic -- a timing bound, the records land in wrong slots
 constexpr bool BIN_FAKE_RESERVE = false;
-// BBF contains: test the k draws in groups of EXIT_GROUP and let a warp stop
-// after a group once none of its 32 keys can still be present (0: off)
-constexpr int EXIT_GROUP = 4;
 }  // namespace tuning
 }  // namespace bf

@@ -130,6 +130,62 @@ def test_every_compiled_schedule_multitile(bflib, cuda, cfg, scheds):
         assert int(out[nw].item()) == -1, "wrote past ceil(n/32) words"
 
 
+def _query_runs(pos, n_neg):
+    """Queries in runs that decide whether a warp's 32 keys can all fail
+    early (the BBF contains' grouped early exit, tuning::EXIT_GROUP): 2^20
+    negatives (all-negative warps: the exit taken), 2^20 negatives with a
+    positive at every index = 13 mod 32 (key slot 1 of lanes 3/11/19/27 of a
+    128-key tile, so some warp calls keep one live lane and the others exit),
+    2^18 positives (no exit), a ragged tail of 1,007 negatives."""
+    neg = synth.negatives(n_neg, offset=4242)
+    a = neg[: 1 << 20]
+    b = neg[1 << 20: 2 << 20].copy()
+    b[13::32] = pos[: b[13::32].size]
+    c = pos[: 1 << 18]
+    d = neg[2 << 20: (2 << 20) + 1007]
+    return np.concatenate([a, b, c, d])
+
+
+BBF_GROUPS = [(c, s) for c, s in GROUPS if c[0] == 1]
+
+
+@pytest.mark.parametrize("cfg,scheds", BBF_GROUPS, ids=[f"v{c[0]}_B{c[1]}_S{c[2]}_k{c[3]}_z{c[4]}" for c, _ in BBF_GROUPS])
+def test_bbf_contains_runs_of_negatives(bflib, cuda, cfg, scheds):
+    """Every compiled BBF contains schedule on the run-structured query of
+    _query_runs, against a half-full filter (every drawn bit set with
+    probability ~1/2, so an all-negative warp fails within a few draw groups
+    while a warp with one positive lane runs all k draws): every result bit
+    equals the oracle's, including the false positives."""
+    import torch
+    bf = bflib
+    v, B, S, k, z = cfg
+    n = 1 << 20
+    b = _odd_blocks(int(n * k / math.log(2)), B)
+    m = b * B
+    keys = _keys(3000, n)
+    query = _query_runs(keys, (2 << 20) + 1007)
+    o = OracleFilter(v, m, B=B, S=S, k=k, z=z)
+    o.add(keys, threads=THREADS)
+    want_res = torch.from_numpy(o.contains(query, threads=THREADS).view(np.int32)).to(cuda)
+    kd, qd = _dev(torch, keys, cuda), _dev(torch, query, cuda)
+    f = bf.Filter(m, k, B, S, variant=v, z=z)
+    f.add(kd)
+    assert torch.equal(f.data(), torch.from_numpy(o.bytes()).to(cuda))
+    out = torch.empty((query.size + 31) // 32 + 1, dtype=torch.int32, device=cuda)
+    ran = 0
+    for op, theta, phi, kpt, hv in scheds:
+        if op != 1:
+            continue
+        f.set_layout(1, theta, phi, kpt, hv)
+        out.fill_(-1)
+        f.contains(qd, out)
+        nw = want_res.numel()
+        assert torch.equal(out[:nw], want_res), f"contains schedule Θ={theta} Φ={phi} kpt={kpt} hv={hv}"
+        assert int(out[nw].item()) == -1, "wrote past ceil(n/32) words"
+        ran += 1
+    assert ran > 0
+
+
 def test_generic_kernel_multitile(bflib, cuda):
     """The runtime-parameter kernel (grid-stride, one key per thread) over
     many grid strides, ragged tail: SBF 512/32 k=16 (no specialization)."""

@@ -68,9 +68,5 @@ constexpr int APPLY_TMA_WARPS = BF_APPLY_TMA_WARPS;
 #define BF_BIN_FAKE_RESERVE 0
 #endif
 constexpr bool BIN_FAKE_RESERVE = BF_BIN_FAKE_RESERVE;
-#ifndef BF_EXIT_GROUP
-#define BF_EXIT_GROUP 0
-#endif
-constexpr int EXIT_GROUP = BF_EXIT_GROUP;
 }  // namespace tuning
 }  // namespace bf
