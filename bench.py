@@ -512,7 +512,7 @@ def _rng_accesses(n, unit):
     return -(-n // unit) * unit
 
 
-def run_probes_l2(bf, torch, cfg, dev, n=1 << 26, sizes=None):
+def run_probes_l2(bf, torch, cfg, dev, n=1 << 26, sizes=None, buf=None):
     """R_read / R_red on a buffer of the filter's size and block geometry
     (SURVEY 8(d) roofline probes), every form measured live on 2^26 keys
     (the asymptotic rate: no launch ramp or tail) and in two launch shapes
@@ -529,10 +529,21 @@ def run_probes_l2(bf, torch, cfg, dev, n=1 << 26, sizes=None):
     so that probe and kernel pay the same per-launch costs (CTA start-up of
     the ~4,700 wave CTAs, ramp, tail: ~11 us per launch measured with
     tools/kexp at any n >= 2^23); these are the `roofline` denominators and the
-    2^26-key ones are reported beside them (`frac_asymptotic`)."""
+    2^26-key ones are reported beside them (`frac_asymptotic`).
+
+    `buf`: the product filter's own word array (a uint8 view; the probes
+    overwrite it after the timed region), so that probe and kernel access the
+    same allocation -- the same physical pages, L2 slices and partitions (the
+    probes on a fresh allocation of the same size measured up to 5% apart
+    from box to box while the product kernels did not)."""
     B = max(64, cfg["B"])
     nbytes = cfg["m_bits"] // 8
-    buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    own = buf is not None
+    if own:
+        assert buf.numel() >= nbytes and buf.dtype == torch.uint8
+        buf = buf[:nbytes]
+    else:
+        buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
     keys = torch.empty(n, dtype=torch.int64, device=dev)
     bf.bf_keygen(keys, n, 0)
     out = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
@@ -584,6 +595,7 @@ def run_probes_l2(bf, torch, cfg, dev, n=1 << 26, sizes=None):
                         + " / ".join(f"{k} {v}" for k, v in read.items()) + " Gkeys/s (form@CTAs per SM)")
     res["red_name"] = (f"R_red^L2(B={B}): {lanes} lanes x RED.64 into one block per key, no hash, 2^26 keys; best of "
                        + " / ".join(f"{k} {v}" for k, v in red.items()) + " Gkeys/s (form@CTAs per SM)")
+    res["buffer"] = "the product filter's own allocation" if own else "a fresh allocation of the filter's size"
     del buf, keys, out, recs
     torch.cuda.empty_cache()
     return res
@@ -775,7 +787,8 @@ def run_ours(a, cfg, rank, world, local_rank):
     probes = None
     if not a.no_probe and rank == 0:
         if cfg["residency"] == "L2":
-            probes = run_probes_l2(bf, torch, cfg, dev, sizes={"add": cfg["n"], "contains": cfg["n"] + cfg["n_neg"]})
+            probes = run_probes_l2(bf, torch, cfg, dev, sizes={"add": cfg["n"], "contains": cfg["n"] + cfg["n_neg"]},
+                                   buf=leg.f.data())
         else:
             probes = run_probes_hbm(bf, torch, cfg, 1 << 28)
     e2e = None
@@ -802,7 +815,8 @@ def run_ours(a, cfg, rank, world, local_rank):
             rr = lg.run(sub_steps, 3, a.graph)
             pr = None
             if not a.no_probe:
-                pr = (run_probes_l2(bf, torch, c, dev, sizes={"add": c["n"], "contains": c["n"] + c["n_neg"]})
+                pr = (run_probes_l2(bf, torch, c, dev, sizes={"add": c["n"], "contains": c["n"] + c["n_neg"]},
+                                    buf=lg.f.data())
                       if c["residency"] == "L2"
                       else run_probes_hbm(bf, torch, c, 1 << 28))
             extra[key] = leg_result(lg, rr, pr, c, world, hbm_peak)

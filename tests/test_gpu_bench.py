@@ -69,3 +69,26 @@ def test_bench_default_legs(cuda):
         assert h["roofline_kernels"]["contains"]["bound"] == "hbm"
         assert h["add_path"] == "binned"
     assert d["fixed_load"]["workload"].startswith("configs[1] fixed load")
+
+
+@pytest.mark.parametrize("merge", ["alltoall", "allgather", "route"])
+def test_bench_under_torchrun(cuda, merge):
+    """The driver's multi-GPU launch form (torch.distributed.run, one rank
+    per GPU, NCCL, rendezvous on 127.0.0.1) at one rank: RANK / LOCAL_RANK /
+    WORLD_SIZE come from the environment, rank 0 prints one contract line
+    with n_gpus = WORLD_SIZE, for each merge strategy."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "1", "--config", "c1", "--steps", "3", "--warmup", "3", "--merge", merge,
+                        "--no-cpu", "--no-e2e", "--no-probe"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["config"]["workload"].startswith("configs[0]")
