@@ -485,6 +485,18 @@ class Leg:
                 "contains_gkeys_s": (n + nneg) / (t["contains"] * 1e-3) / 1e9,
                 "fp": fp}
 
+    def phase_pass(self):
+        """One eager step with the library's phase timing on, after the timed
+        region (bf_set_phase_timing: CUDA events around each binned phase's
+        launches on the stream that runs them): {phase: (ms, spans)}."""
+        f = self.f
+        f.set_phase_timing(True)
+        self.step()
+        self.torch.cuda.synchronize()
+        t = f.phase_times()
+        f.set_phase_timing(False)
+        return t
+
     def free(self):
         del self.f, self.q, self.keys, self.out
         self.torch.cuda.empty_cache()
@@ -638,6 +650,78 @@ def run_probes_hbm(bf, torch, cfg, n):
     return res
 
 
+def run_probes_range(bf, torch, cfg, buf, n=1 << 26):
+    """The L2 bounds of the binned paths' per-range kernels, on views of the
+    product filter's own allocation (after the timed region): the apply ORs
+    records into one L2-resident range of the binned add (32 MiB, the
+    library default) -- R_red of that range (LSU REDs of the block's lanes,
+    and the LSU+TMA form); the lookup tests records against one range of the
+    binned contains (64 MiB) -- R_read of that range (in-register block
+    loads).  Launch shapes 8 and 32 CTAs/SM; the best form is the bound."""
+    B = cfg["B"]
+    lanes = max(1, B // 64)
+    sms = torch.cuda.get_device_properties(buf.device).multi_processor_count
+    res = {}
+    for name, mib in (("apply_range", 32), ("lookup_range", 64)):
+        view = buf[: mib << 20]
+        b = (mib << 20) * 8 // B
+        forms = {}
+        for cps in (8, 32):
+            bf.bf_set_probe_launch(cps)
+            thr = sms * cps * 256
+            if name == "apply_range":
+                fl = {"red_rng": (lambda: bf.bf_probe_rng(view, b, B, 1, lanes, n), _rng_accesses(n, thr // lanes))}
+                if B >= 128:
+                    fl["red_lsu_tma"] = (lambda: bf.bf_probe_rng(view, b, B, 3, lanes, n), _rng_accesses(n, thr))
+            else:
+                fl = {"read_rng": (lambda: bf.bf_probe_rng(view, b, B, 0, 1, n), _rng_accesses(n, thr * 4))}
+            for fn_name, (fn, acc) in fl.items():
+                forms[f"{fn_name}@{cps}"] = round(acc / (best_time(torch, fn) * 1e-3) / 1e9, 3)
+        bf.bf_set_probe_launch(0)
+        best = max(forms, key=forms.get)
+        res[name] = {"range_mib": mib, "forms": forms, "best": forms[best], "best_form": best}
+    return res
+
+
+def phase_rooflines(phases, range_probes, cfg, hbm_peak):
+    """Each binned phase against its own bound: bin / bin-with-slots / unbin
+    against HBM streaming (their algorithmic bytes per key over the measured
+    copy peak), apply / lookup against the L2 probe of their range
+    (run_probes_range) in Gkeys/s, shown as GB/s of 32-byte sectors."""
+    n, nneg = cfg["n"], cfg["n_neg"]
+    nq = n + nneg
+    out = {}
+    spec = {"bin": (n, 16.0, "hbm", "key 8 B in + record 8 B out"),
+            "apply": (n, None, "l2", "apply_range"),
+            "bin_slots": (nq, 20.0, "hbm", "key 8 B in + record 8 B + slot 4 B out"),
+            "lookup": (nq, None, "l2", "lookup_range"),
+            "unbin": (nq, 4.125, "hbm", "slot 4 B in + 1/8 B result out (+ the result-bit gather from L2)")}
+    for ph, (keys, bpk, bound, what) in spec.items():
+        ms, spans = phases.get(ph, (0.0, 0))
+        if spans == 0 or ms <= 0:
+            continue
+        g = keys / (ms * 1e-3) / 1e9
+        o = {"bound": bound, "ms": round(ms, 4), "spans": spans, "achieved_gkeys_s": round(g, 3)}
+        if bound == "hbm":
+            o.update({"achieved": round(g * bpk, 1), "peak": hbm_peak, "unit": "GB/s",
+                      "frac": round(g * bpk / hbm_peak, 4), "algorithmic_bytes_per_key": bpk,
+                      "peak_kind": "MEASURED_PEAKS.json hbm_gbs (copy)", "bytes": what})
+        else:
+            pr = range_probes[what]
+            o.update({"achieved": round(g * 32, 1), "peak": round(pr["best"] * 32, 1), "unit": "GB/s",
+                      "frac": round(g / pr["best"], 4), "algorithmic_bytes_per_key": 32,
+                      "peak_gkeys_s": pr["best"],
+                      "peak_kind": f"measured live: L2 probe on a {pr['range_mib']} MiB range of the filter's own "
+                                   f"allocation, best of {pr['forms']}"})
+        out[ph] = o
+    return out
+
+
+PHASE_KERNELS = {"bin": "bin_range_kernel", "apply": "apply_kernel, one launch per range",
+                 "bin_slots": "bin_range_kernel<..., SLOTS>", "lookup": "lookup_kernel, one launch per range",
+                 "unbin": "unbin_kernel"}
+
+
 def sector_bytes(B):
     return max(32, B // 8)
 
@@ -766,6 +850,17 @@ def leg_result(leg, r, probes, cfg, world, hbm_peak):
         res["roofline"] = ka if dom == "add" else kc
         res["roofline_kernels"] = {"add": ka, "contains": kc}
         res["probes"] = probes
+        if r.get("phases") and r.get("range_probes"):
+            ph = phase_rooflines(r["phases"], r["range_probes"], cfg, hbm_peak)
+            if ph:
+                # the step's dominant kernel is the phase with the most time:
+                # it carries the leg's roofline; the whole-path streaming
+                # figures stay in roofline_kernels
+                top = max(ph, key=lambda k: ph[k]["ms"])
+                res["roofline_phases"] = ph
+                res["roofline"] = dict(ph[top], kernel=f"{top} phase ({PHASE_KERNELS[top]})",
+                                       traffic=None, dominant_by="phase time in one eager step (bf_phase_times)")
+                res["range_probes"] = r["range_probes"]
     return res
 
 
@@ -784,6 +879,10 @@ def run_ours(a, cfg, rank, world, local_rank):
     leg = Leg(bf, torch, cfg, a, rank, world, dev, bfdist)
     with ClockSampler(local_rank) as clk:
         r = leg.run(a.steps, a.warmup, a.graph, clk)
+    if cfg["residency"] == "HBM":
+        r["phases"] = leg.phase_pass()
+        if not a.no_probe and rank == 0:
+            r["range_probes"] = run_probes_range(bf, torch, cfg, leg.f.data())
     probes = None
     if not a.no_probe and rank == 0:
         if cfg["residency"] == "L2":
@@ -813,6 +912,10 @@ def run_ours(a, cfg, rank, world, local_rank):
                 continue
             lg = Leg(bf, torch, c, a, rank, world, dev, bfdist)
             rr = lg.run(sub_steps, 3, a.graph)
+            if c["residency"] == "HBM":
+                rr["phases"] = lg.phase_pass()
+                if not a.no_probe:
+                    rr["range_probes"] = run_probes_range(bf, torch, c, lg.f.data())
             pr = None
             if not a.no_probe:
                 pr = (run_probes_l2(bf, torch, c, dev, sizes={"add": c["n"], "contains": c["n"] + c["n_neg"]},

@@ -214,6 +214,24 @@ int bf_set_contains_mode(bf_filter* f, int mode);
 /* mode set by bf_set_contains_mode, and whether the most recent bf_contains was binned. */
 int bf_get_contains_mode(const bf_filter* f, int* mode, int* last_binned);
 
+/* Phase timing of the binned paths (measurement, not part of the paper's
+ * method: it lets a benchmark give each phase kernel its own roofline,
+ * DESIGN.md section 7).  While on, every binned bf_add / bf_contains on this
+ * filter records a pair of CUDA timing events around each phase's launches on
+ * the stream that runs them (nothing is recorded under stream capture).
+ * bf_phase_times synchronizes on those events, writes the summed milliseconds
+ * per phase to ms[BF_PHASES] and the number of timed spans (batches) to
+ * spans[BF_PHASES] (may be NULL), and forgets them.  BF_EINVAL on a NULL
+ * filter or ms; BF_ECUDA if an event failed (the others are still summed). */
+enum { BF_PHASE_BIN = 0,        /* binned add: range binning (bin_range_kernel) */
+       BF_PHASE_APPLY = 1,      /* binned add: the per-range apply launches */
+       BF_PHASE_BIN_SLOTS = 2,  /* binned contains: range binning with key slots */
+       BF_PHASE_LOOKUP = 3,     /* binned contains: the per-range lookup launches */
+       BF_PHASE_UNBIN = 4,      /* binned contains: result bits back to key order */
+       BF_PHASES = 5 };
+int bf_set_phase_timing(bf_filter* f, int on);
+int bf_phase_times(bf_filter* f, double* ms, uint64_t* spans);
+
 /* Current schedule of `op` and whether it runs a specialized (compile-time
  * k/B/S) kernel (1) or the generic runtime-parameter kernel (0). */
 int bf_get_layout(const bf_filter* f, int op, int* theta, int* phi, int* kpt,

@@ -70,6 +70,8 @@ _SIGS = {
     "bf_get_add_mode": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
     "bf_set_contains_mode": (_i32, [_vp, _i32]),
     "bf_get_contains_mode": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
+    "bf_set_phase_timing": (_i32, [_vp, _i32]),
+    "bf_phase_times": (_i32, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "bf_create_part": (_vp, [_u64, _u32, _u32, _u32, _u32, _u64, _u32, _u32]),
     "bf_part_info": (_i32, [_vp, C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u64), C.POINTER(_u64),
                             C.POINTER(_u64)]),
@@ -270,6 +272,21 @@ def bf_get_contains_mode(f: int) -> tuple[int, int]:
     m, last = C.c_int(0), C.c_int(0)
     _check(_lib.bf_get_contains_mode(f, C.byref(m), C.byref(last)))
     return m.value, last.value
+
+
+BF_PHASE_NAMES = ("bin", "apply", "bin_slots", "lookup", "unbin")  # include/bf.h BF_PHASE_*
+
+
+def bf_set_phase_timing(f: int, on: bool) -> None:
+    _check(_lib.bf_set_phase_timing(f, 1 if on else 0))
+
+
+def bf_phase_times(f: int) -> dict:
+    """{phase: (milliseconds, spans)} of the binned phases timed since the last call."""
+    n = len(BF_PHASE_NAMES)
+    ms, spans = (C.c_double * n)(), (C.c_uint64 * n)()
+    _check(_lib.bf_phase_times(f, ms, spans))
+    return {name: (float(ms[i]), int(spans[i])) for i, name in enumerate(BF_PHASE_NAMES)}
 
 
 def bf_or_fold(dst, srcs, nsrc: int, src_stride_bytes: int, nbytes: int, stream=None) -> None:
@@ -502,6 +519,12 @@ class Filter:
     def contains_mode(self) -> tuple[int, int]:
         """(mode, whether the last contains took the binned path)."""
         return bf_get_contains_mode(self.handle)
+
+    def set_phase_timing(self, on: bool):
+        bf_set_phase_timing(self.handle, on)
+
+    def phase_times(self) -> dict:
+        return bf_phase_times(self.handle)
 
     def add_mode(self) -> tuple[int, int]:
         """(mode, whether the last add took the binned path)."""

@@ -10,6 +10,8 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <utility>
+#include <vector>
 
 #include "../../include/bf.h"
 #include "bf_internal.h"
@@ -173,6 +175,10 @@ struct bf_filter {
     // binned adds issued on different streams
     std::mutex mu;
     cudaEvent_t scratch_done;
+    // phase timing of the binned paths (bf_set_phase_timing; measurement
+    // only): event pairs recorded around each phase's launches
+    int phase_on;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> phase_ev;
     int ctas_per_sm[2];  // bf_set_launch: 0 = occupancy (default)
 };
 
@@ -432,6 +438,10 @@ void bf_destroy(bf_filter* f)
         if (f->ev_apply[i]) cudaEventDestroy(f->ev_apply[i]);
     }
     if (f->side) cudaStreamDestroy(f->side);
+    for (auto& pe : f->phase_ev) {
+        cudaEventDestroy(pe.second.first);
+        cudaEventDestroy(pe.second.second);
+    }
     cudaFree(f->words);
     delete f;
 }
@@ -579,6 +589,31 @@ static bool binned_available(const bf_filter* f, KernelFn* bin, KernelFn* apply)
 static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cudaStream_t st, KernelFn bin_fn,
                              KernelFn apply_fn);
 
+// Phase timing (bf_set_phase_timing): phase_begin records a start event on
+// st and returns its index in f->phase_ev, phase_end the matching stop event.
+// Off (or under stream capture) both are no-ops.  Events are created per
+// call: a measurement pass, never the timed product path.
+static int phase_begin(bf_filter* f, int phase, cudaStream_t st)
+{
+    if (!f->phase_on) return -1;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return -1;
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) {
+        if (a) cudaEventDestroy(a);
+        cudaGetLastError();
+        return -1;
+    }
+    cudaEventRecord(a, st);
+    f->phase_ev.push_back({phase, {a, b}});
+    return (int)f->phase_ev.size() - 1;
+}
+
+static void phase_end(bf_filter* f, int idx, cudaStream_t st)
+{
+    if (idx >= 0) cudaEventRecord(f->phase_ev[idx].second.second, st);
+}
+
 static int binned_add(bf_filter* f, const uint64_t* keys, uint64_t n, cudaStream_t st, KernelFn bin_fn,
                       KernelFn apply_fn)
 {
@@ -700,9 +735,11 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         void* args[] = {&bp};
         uint64_t chunks = (cnt + BIN_CHUNK - 1) / BIN_CHUNK;
         const unsigned gb = (unsigned)(chunks < (uint64_t)grid_bin ? chunks : grid_bin);
+        const int pb = phase_begin(f, BF_PHASE_BIN, st);
         if ((e = cudaLaunchKernel((const void*)bin_fn, dim3(gb), dim3(BIN_THREADS), args, smem, st)) != cudaSuccess)
             return cuda_fail(e, "bin launch");
         if (int rc = check_launch("bin launch")) return rc;
+        phase_end(f, pb, st);
         if (side != st && ((e = cudaEventRecord(f->ev_bin[buf], st)) != cudaSuccess ||
                            (e = cudaStreamWaitEvent(side, f->ev_bin[buf], 0)) != cudaSuccess))
             return cuda_fail(e, "binned add: bin -> apply");
@@ -710,12 +747,14 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         const uint64_t tiles = (cap + 32 * f->sched[0].kpt - 1) / (32 * f->sched[0].kpt);
         uint64_t ga = (tiles + 7) / 8;
         if (ga > (uint64_t)grid_apply) ga = grid_apply;
+        const int pa = phase_begin(f, BF_PHASE_APPLY, side);
         for (uint32_t r = 0; r < (uint32_t)R; ++r) {
             bp.range = r;
             if ((e = launch_range_kernel(apply_fn, (unsigned)ga, args, side, r > 0)) != cudaSuccess)
                 return cuda_fail(e, "apply launch");
             if (int rc = check_launch("apply launch")) return rc;
         }
+        phase_end(f, pa, side);
         if (side != st && (e = cudaEventRecord(f->ev_apply[buf], side)) != cudaSuccess)
             return cuda_fail(e, "binned add: apply event");
     }
@@ -815,26 +854,32 @@ static int binned_contains_locked(bf_filter* f, const uint64_t* keys, uint64_t n
         void* args[] = {&bp};
         const uint64_t chunks = (cnt + BIN_CHUNK - 1) / BIN_CHUNK;
         const unsigned gb = (unsigned)(chunks < (uint64_t)waves ? chunks : waves);
+        const int pb = phase_begin(f, BF_PHASE_BIN_SLOTS, st);
         if ((e = cudaLaunchKernel((const void*)bin_fn, dim3(gb), dim3(BIN_THREADS), args, smem, st)) != cudaSuccess)
             return cuda_fail(e, "binned contains: bin launch");
         if ((rc = check_launch("binned contains: bin launch"))) return rc;
+        phase_end(f, pb, st);
         const uint64_t tiles = (cap + 32 * LOOKUP_RPL - 1) / (32 * LOOKUP_RPL);
         uint64_t gl = (tiles + 7) / 8;
         if (gl > (uint64_t)kLookupCtasPerSm * sm_count(f->device)) gl = (uint64_t)kLookupCtasPerSm * sm_count(f->device);
+        const int pl = phase_begin(f, BF_PHASE_LOOKUP, st);
         for (uint32_t r = 0; r < (uint32_t)R; ++r) {  // one launch per range: the GPU stays in one L2-resident range
             bp.range = r;
             if ((e = launch_range_kernel(look_fn, (unsigned)gl, args, st, r > 0)) != cudaSuccess)
                 return cuda_fail(e, "binned contains: lookup launch");
             if ((rc = check_launch("binned contains: lookup launch"))) return rc;
         }
+        phase_end(f, pl, st);
         uint32_t* o = out + off / 32;  // off is a multiple of 128
         void* uargs[] = {&bp, &o};
         uint64_t gu = ((cnt + 32 * UNBIN_KPL - 1) / (32 * UNBIN_KPL) + 7) / 8;
         if (gu > (uint64_t)waves) gu = waves;
+        const int pu = phase_begin(f, BF_PHASE_UNBIN, st);
         if ((e = cudaLaunchKernel((const void*)unbin_fn, dim3((unsigned)(gu ? gu : 1)), dim3(256), uargs, 0, st)) !=
             cudaSuccess)
             return cuda_fail(e, "binned contains: unbin launch");
         if ((rc = check_launch("binned contains: unbin launch"))) return rc;
+        phase_end(f, pu, st);
     }
     return BF_OK;
 }
@@ -967,6 +1012,38 @@ int bf_get_contains_mode(const bf_filter* f, int* mode, int* last_binned)
     if (mode) *mode = f->contains_mode;
     if (last_binned) *last_binned = f->last_contains_binned;
     return BF_OK;
+}
+
+int bf_set_phase_timing(bf_filter* f, int on)
+{
+    if (!f) return fail(BF_EINVAL, "null filter");
+    std::lock_guard<std::mutex> g(f->mu);
+    f->phase_on = on ? 1 : 0;
+    return BF_OK;
+}
+
+int bf_phase_times(bf_filter* f, double* ms, uint64_t* spans)
+{
+    if (!f || !ms) return fail(BF_EINVAL, "bf_phase_times: null argument");
+    std::lock_guard<std::mutex> g(f->mu);
+    DeviceGuard dg(f->device);
+    for (int i = 0; i < BF_PHASES; ++i) {
+        ms[i] = 0.0;
+        if (spans) spans[i] = 0;
+    }
+    int rc = BF_OK;
+    for (auto& pe : f->phase_ev) {
+        float t = 0.f;
+        cudaError_t e = cudaEventSynchronize(pe.second.second);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t, pe.second.first, pe.second.second);
+        if (e != cudaSuccess && rc == BF_OK) rc = cuda_fail(e, "bf_phase_times");
+        ms[pe.first] += t;
+        if (spans) ++spans[pe.first];
+        cudaEventDestroy(pe.second.first);
+        cudaEventDestroy(pe.second.second);
+    }
+    f->phase_ev.clear();
+    return rc;
 }
 
 // ------------------------------------------------------------ routing (NEXT N1)

@@ -196,6 +196,12 @@ def test_null_handle_calls_fail_cleanly(bflib):
     L.bf_get_contains_mode.restype = ctypes.c_int
     L.bf_get_contains_mode.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     assert L.bf_get_contains_mode(None, None, None) == bflib.BF_EINVAL
+    L.bf_set_phase_timing.restype = ctypes.c_int
+    L.bf_set_phase_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    assert L.bf_set_phase_timing(None, 1) == bflib.BF_EINVAL
+    L.bf_phase_times.restype = ctypes.c_int
+    L.bf_phase_times.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    assert L.bf_phase_times(None, None, None) == bflib.BF_EINVAL
     L.bf_destroy.argtypes = [ctypes.c_void_p]
     L.bf_destroy(None)  # NULL-safe
     assert bflib.last_error()[0] in (bflib.BF_EINVAL, bflib.BF_OK)

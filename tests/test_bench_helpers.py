@@ -59,3 +59,24 @@ def test_rng_probe_access_rounding_and_roofline_fields():
     r = B.kernel_roofline("bf_contains", 200.0, 250.0, "probe", 256)
     assert r["bound"] == "l2" and r["unit"] == "GB/s" and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
     assert r["algorithmic_bytes_per_key"] == 32
+
+
+def test_phase_rooflines():
+    """Each binned phase against its own bound: streaming phases divide the
+    algorithmic bytes rate by the copy peak, the per-range phases their key
+    rate by the range probe; phases without a timed span are left out."""
+    cfg = {"n": 1 << 32, "n_neg": 1 << 28}
+    phases = {"bin": (20.0, 2), "apply": (35.0, 2), "bin_slots": (25.0, 3), "lookup": (22.0, 3), "unbin": (0.0, 0)}
+    probes = {"apply_range": {"range_mib": 32, "forms": {"red_rng@32": 128.0}, "best": 128.0, "best_form": "red_rng@32"},
+              "lookup_range": {"range_mib": 64, "forms": {"read_rng@32": 270.0}, "best": 270.0,
+                               "best_form": "read_rng@32"}}
+    r = B.phase_rooflines(phases, probes, cfg, 6500.0)
+    assert set(r) == {"bin", "apply", "bin_slots", "lookup"}
+    g_bin = (1 << 32) / 20e-3 / 1e9
+    assert abs(r["bin"]["achieved_gkeys_s"] - round(g_bin, 3)) < 1e-3
+    assert abs(r["bin"]["frac"] - round(g_bin * 16 / 6500.0, 4)) < 1e-4 and r["bin"]["bound"] == "hbm"
+    g_app = (1 << 32) / 35e-3 / 1e9
+    assert r["apply"]["bound"] == "l2" and abs(r["apply"]["frac"] - round(g_app / 128.0, 4)) < 1e-4
+    g_look = ((1 << 32) + (1 << 28)) / 22e-3 / 1e9
+    assert abs(r["lookup"]["frac"] - round(g_look / 270.0, 4)) < 1e-4
+    assert abs(r["bin_slots"]["frac"] - round(((1 << 32) + (1 << 28)) / 25e-3 / 1e9 * 20 / 6500.0, 4)) < 1e-4

@@ -433,6 +433,42 @@ def test_binned_contains_matches_oracle(bflib, cuda, cfg, range_bytes, batch, mi
     assert np.array_equal(got, o.contains(q))
 
 
+def test_phase_timing_of_binned_paths(bflib, cuda):
+    """bf_set_phase_timing / bf_phase_times (measurement hook): one timed span
+    per batch and phase, positive times, nothing recorded while off or for
+    direct calls, and the timed binned add / contains still match the
+    oracle."""
+    import torch
+    bf = bflib
+    v, B, S, k, z = 3, 256, 64, 8, 0
+    m = (1 << 22) + 5 * B
+    keys = synth.keys(777, 100_003)
+    q = np.concatenate([keys[:50_000], synth.negatives(50_011)])
+    o = OracleFilter(v, m, B=B, S=S, k=k, z=z)
+    o.add(keys)
+    f = bf.Filter(m, k, B, S, variant=v, z=z)
+    f.set_add_mode(bf.BF_ADD_BINNED, 1 << 16, 40_000)  # 3 batches of keys, 3 of queries
+    f.set_contains_mode(bf.BF_CONTAINS_BINNED)
+    kd, qd = _to_dev(torch, keys, cuda), _to_dev(torch, q, cuda)
+    f.add(kd)  # not timed
+    assert all(t == (0.0, 0) for t in f.phase_times().values())
+    f.clear()
+    f.set_phase_timing(True)
+    f.add(kd)
+    got = _gpu_contains(torch, f, qd)
+    t = f.phase_times()
+    assert t["bin"][1] == 3 and t["apply"][1] == 3, t
+    assert t["bin_slots"][1] == 3 and t["lookup"][1] == 3 and t["unbin"][1] == 3, t
+    assert all(ms > 0 for ms, _ in t.values()), t
+    assert np.array_equal(_gpu_bytes(f), o.bytes())
+    assert np.array_equal(got, o.contains(q))
+    assert all(v == (0.0, 0) for v in f.phase_times().values())  # forgotten after reading
+    f.set_add_mode(bf.BF_ADD_DIRECT)
+    f.add(kd)  # the direct path records nothing
+    assert all(v == (0.0, 0) for v in f.phase_times().values())
+    f.set_phase_timing(False)
+
+
 def test_binned_contains_bucket_overflow(bflib, cuda):
     """Queries concentrated in one range overflow its bucket; those keys are
     looked up directly (slot marker) and every answer is still exact."""
