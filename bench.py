@@ -947,11 +947,16 @@ def run_ours(a, cfg, rank, world, local_rank):
         "fpr": main["fpr"],
         "roofline": main.get("roofline"),
         "roofline_kernels": main.get("roofline_kernels"),
+        "roofline_phases": main.get("roofline_phases"),
+        "range_probes": main.get("range_probes"),
         "hbm_context": main.get("hbm_context"),
         "probes": main.get("probes"),
         "gpu_launches": main["gpu_launches"],
         "clocks": clk.summary(),
     }
+    for key in ("roofline_phases", "range_probes"):
+        if res[key] is None:
+            del res[key]
     res.update(extra)
     if e2e:
         res["e2e"] = e2e

@@ -4,8 +4,10 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <string>
@@ -589,6 +591,21 @@ static bool binned_available(const bf_filter* f, KernelFn* bin, KernelFn* apply)
 static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cudaStream_t st, KernelFn bin_fn,
                              KernelFn apply_fn);
 
+// The apply launch of range r prefetches range r + 1 into L2
+// (bf_binned.cuh prefetch_next_range).
+static void set_prefetch(const bf_filter* f, BinParams& bp, uint32_t r, uint32_t lg, uint64_t R)
+{
+    bp.pf_off = bp.pf_bytes = 0;
+    if (r + 1 >= R) return;
+    const uint64_t blk_bytes = f->B / 8;
+    const uint64_t lo = ((uint64_t)(r + 1) << lg) * blk_bytes;
+    const uint64_t hi = std::min(((uint64_t)(r + 2) << lg) * blk_bytes, f->b * blk_bytes);
+    if (hi > lo) {
+        bp.pf_off = lo;
+        bp.pf_bytes = hi - lo;
+    }
+}
+
 // Phase timing (bf_set_phase_timing): phase_begin records a start event on
 // st and returns its index in f->phase_ev, phase_end the matching stop event.
 // Off (or under stream capture) both are no-ops.  Events are created per
@@ -750,6 +767,7 @@ static int binned_add_locked(bf_filter* f, const uint64_t* keys, uint64_t n, cud
         const int pa = phase_begin(f, BF_PHASE_APPLY, side);
         for (uint32_t r = 0; r < (uint32_t)R; ++r) {
             bp.range = r;
+            set_prefetch(f, bp, r, lg, R);
             if ((e = launch_range_kernel(apply_fn, (unsigned)ga, args, side, r > 0)) != cudaSuccess)
                 return cuda_fail(e, "apply launch");
             if (int rc = check_launch("apply launch")) return rc;

@@ -47,7 +47,35 @@ struct BinParams {
     // 0xFFFFFFFF = its bucket was full) and one result bit per record slot
     uint32_t* slot_out;
     uint32_t* res_bits;
+    // phase 2: the next range's bytes of the filter (pf_bytes = 0: none),
+    // prefetched into L2 while this range is applied / looked up
+    uint64_t pf_off;
+    uint64_t pf_bytes;
 };
+
+// Each CTA of a per-range apply launch asks the TMA engine to prefetch its
+// slice of the NEXT range into L2 (cp.async.bulk.prefetch.L2: a hint, no data
+// moves into the SM), so that range's first touches hit L2 instead of DRAM.
+// Measured on configs[2] (profiles/ab_pf_next_r3): binned add 80.7 -> 82.8
+// Gkeys/s with the 32 MiB add ranges; the binned contains' lookup does not
+// gain at 32 MiB ranges (89.6 -> 89.2) and loses at its 64 MiB default
+// (89.4 -> 84.0: two 64 MiB ranges do not fit the 126 MB L2), so it does not
+// prefetch.
+__device__ __forceinline__ void prefetch_next_range(const BinParams& bp)
+{
+    if (bp.pf_bytes == 0 || threadIdx.x != 0) return;
+    const uint64_t per = ((bp.pf_bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ULL;
+    const uint64_t off = (uint64_t)blockIdx.x * per;
+    if (off >= bp.pf_bytes) return;
+    uint64_t len = min(per, bp.pf_bytes - off);
+    const char* p = (const char*)bp.f.words + bp.pf_off + off;
+    while (len >= 16) {
+        const uint32_t c = (uint32_t)min(len, (uint64_t)(1u << 20)) & ~15u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(c) : "memory");
+        p += c;
+        len -= c;
+    }
+}
 
 // Programmatic dependent launch of the per-range kernels (apply, lookup):
 // ranges are independent (OR commutes; a lookup reads the filter and writes
@@ -725,6 +753,7 @@ __global__ void __launch_bounds__(256) apply_kernel(const BinParams bp)
     using W = typename C::W;
     constexpr int KPT = C::KPT;
     pdl_launch_dependents();
+    prefetch_next_range(bp);
     constexpr uint64_t TILE = 32 * KPT;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t pos = lane & (uint32_t)(C::THETA - 1);
